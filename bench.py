@@ -1,0 +1,388 @@
+"""bench.py -- TF-edit DVL update throughput on B200 (BASELINE.json metric).
+
+A "step" is one transfer-function edit through the whole TF-update path (U0-U6 of
+SURVEY.md 8(a)): dvl_update_tf(member 0, new TF) + dvl_get_polylines(W).  The build
+(B0-B3: ingest, Hilbert encode, onesweep sort, gather) runs once per dataset; it is timed
+separately over its own repetitions and reported in the same JSON line ("build").
+
+Workload at N=1: BASELINE.json configs[1] (C2: synthetic 3-level AMR, ~10.9 M cells,
+4 members, W=1024, repeated TF edits on member 0).  Inputs are resident in HBM; L2 is
+flushed (256 MiB write) before every timed step.  Device time per step = CUDA events on
+the library's stream; per-kernel times come from the library's own events (same stream).
+
+--impl reference times the CPU oracle (oracle/, single thread) on the same config.
+N>1 (torchrun): every rank runs the workload on its own GPU (replicas, weak scaling);
+timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TF-edit DVL update ms & Gcells/s at 1/2/4/8 B200; build (Hilbert+sort) ms"
+CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--build-reps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.stop_ = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self.stop_.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def workload(name):
+    import synth
+    c = synth.make_config(name)
+    return c
+
+
+def tf_sequence(cfg_name, count, N, M):
+    import synth
+    ci = CONFIG_INDEX[cfg_name]
+    base = [synth.tf_edit(ci, 0, N, member=m) for m in range(M)]
+    edits = [synth.tf_edit(ci, 1 + e, N, member=0) for e in range(count)]
+    return base, edits
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+# ----------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as o
+    c = workload(args.config)
+    n_full = len(c["level"])
+    M, W = c["M"], c["W"]
+    base, edits = tf_sequence(args.config, args.warmup + args.steps, 256, M)
+    tfs = np.stack(base)
+    B = o.build(c["lower"], c["level"], c["scal"])
+    # bounded sample: keep the whole run within a few minutes
+    t0 = time.perf_counter()
+    o.update(B, tfs, W, domain=c["domain"])
+    t_one = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    frac = min(1.0, budget / max(t_one, 1e-9))
+    if frac < 1.0:
+        k = max(1, int(n_full * frac))
+        B = o.Built(k, B.M, B.E, B.b, B.Lmax, B.codes[:k], B.perm[:k], B.level_s[:k],
+                    np.ascontiguousarray(B.scal_s[:, :k]), B.vmin, B.vmax)
+    n = B.n
+    times = []
+    for e in range(args.warmup + args.steps):
+        tfs[0] = edits[e]
+        t0 = time.perf_counter()
+        o.update(B, tfs, W, domain=c["domain"], n_global=n_full)
+        dt = time.perf_counter() - t0
+        if e >= args.warmup:
+            times.append(dt)
+    sec = sum(times) / len(times)
+    value = n / sec / 1e9
+    sample = f"{n} of {n_full} curve-ordered cells of {args.config}, full TF-update pipeline per step"
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": "Gcells/s",
+          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/u64",
+          "data": "synthetic",
+          "config": {"workload": f"{args.config}: synthetic AMR ensemble, {n_full} cells, M={M}, W={W}",
+                     "members": M, "W": W},
+          "cpu_baseline": {"value": value, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
+                           "sample": sample},
+          "e2e": {"value": value, "unit": "Gcells/s", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 0}})
+
+
+# -------------------------------------------------------------------------- native arm
+def cpu_baseline(c, edits_base, W, budget_s=20.0):
+    """The oracle as it stands, single-threaded, on a bounded sample of the workload."""
+    from oracle import oracle as o
+    n_full = len(c["level"])
+    t0 = time.perf_counter()
+    B = o.build(c["lower"], c["level"], c["scal"])
+    t_build = time.perf_counter() - t0
+    tfs = np.stack(edits_base)
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(times) < 10:
+        t0 = time.perf_counter()
+        o.update(B, tfs, W, domain=c["domain"])
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    return {"value": n_full / sec / 1e9, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
+            "sample": f"{len(times)} full TF-update passes of {args_cfg_name} ({n_full} cells), "
+                      f"median; oracle build {t_build:.2f} s"}
+
+
+args_cfg_name = "C2"
+
+
+def run_native(args, rank, world, local):
+    import torch
+    import paper_2306_11612_b200 as dvl
+
+    global args_cfg_name
+    args_cfg_name = args.config
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c = workload(args.config)
+    n = len(c["level"])
+    M, W, N = c["M"], c["W"], 256
+    base, edits = tf_sequence(args.config, args.warmup + args.steps, N, M)
+
+    stream = torch.cuda.Stream()
+    ctx = dvl.Context(device=local, stream=stream, timing=True)
+    dev = torch.device("cuda", local)
+    lower_d = torch.from_numpy(c["lower"].view(np.int32)).to(dev)
+    level_d = torch.from_numpy(c["level"]).to(dev)
+    scal_d = torch.from_numpy(c["scal"]).to(dev)
+    torch.cuda.synchronize()
+
+    # ---- build (device-resident inputs), timed separately
+    build_ms, phase = [], []
+    for r in range(args.build_reps + 1):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        ctx.build(lower_d, level_d, scal_d)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if r > 0:
+            build_ms.append(ev0.elapsed_time(ev1))
+            phase.append(ctx.timings())
+    info = ctx.info()
+    for m in range(M):
+        if c["domain"] is not None:
+            ctx.set_domain(m, float(c["domain"][m, 0]), float(c["domain"][m, 1]))
+        ctx.update_tf(m, base[m])
+    out_d = torch.empty(M * W * 8, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ctx.get_polylines(W, out=out_d)
+    torch.cuda.synchronize()
+
+    def step(e, device_out=True):
+        ctx.update_tf(0, edits[e])
+        if device_out:
+            ctx.get_polylines(W, out=out_d)
+        else:
+            return ctx.get_polylines(W)
+
+    # ---- warm-up
+    for e in range(args.warmup):
+        step(e)
+    torch.cuda.synchronize()
+
+    # ---- timed device steps
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    kern = {"maxv_ms": 0.0, "weights_scan_ms": 0.0, "bin_reduce_ms": 0.0, "epilogue_ms": 0.0}
+    launches = 0
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xff)
+            evs[k][0].record(stream)
+            ctx.update_tf(0, edits[args.warmup + k])
+            t_up = ctx.timings()
+            ctx.get_polylines(W, out=out_d)
+            evs[k][1].record(stream)
+            t_pl = ctx.timings()
+            launches += t_up["launches"] + t_pl["launches"]
+            for key in kern:
+                kern[key] += t_pl[key]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * n / (ms_per_step / 1e3) / 1e9
+
+    # ---- end-to-end through the public API with host buffers (TF H2D, vertices D2H)
+    e2e_times = []
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xff)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.update_tf(0, edits[args.warmup + k])
+        res = ctx.get_polylines(W)   # host output: synchronises
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * sum(e2e_times) / len(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert res["count"].sum() >= n
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (algorithmic bytes, design D2)
+    peak, peak_src = load_peaks()
+    per_kernel = {k: v / args.steps for k, v in kern.items()}
+    bytes_cell = {"weights_scan_ms": 4 * M + 1, "bin_reduce_ms": 4 * M + 1}
+    dom = max(bytes_cell, key=lambda k: per_kernel[k])
+    alg_bytes = n * bytes_cell[dom]
+    achieved = alg_bytes / (per_kernel[dom] / 1e3) / 1e9
+    kname = {"weights_scan_ms": "weights_scan_kernel", "bin_reduce_ms": "bin_reduce_kernel"}[dom]
+    traffic = load_traffic(kname)
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "bytes_per_cell": bytes_cell[dom]}
+    pass_bytes = n * (4 * M + 1) * 2
+    update_kernels_ms = per_kernel["weights_scan_ms"] + per_kernel["bin_reduce_ms"]
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline(c, base, W)
+        except Exception as ex:  # pragma: no cover
+            cpu = {"error": str(ex)}
+    bphase = {k: statistics.median([p[k] for p in phase]) for k in
+              ("ingest_ms", "encode_ms", "sort_ms", "gather_ms")}
+    emit({
+        "metric": METRIC, "value": value, "unit": "Gcells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32/u64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: synthetic 3-level AMR ensemble (BASELINE configs[1])",
+                   "n_cells": n, "members": M, "W": W, "tf_size": N, "levels": int(info["Lmax"]) + 1,
+                   "bits": info["bits"], "edits": "member 0, new random TF per step",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
+                    "p90": float(np.percentile(step_ms, 90))},
+        "kernels_ms": per_kernel,
+        "update_kernels_hbm_gbs": pass_bytes / (update_kernels_ms / 1e3) / 1e9,
+        "build": {"ms": statistics.median(build_ms), "hilbert_sort_ms": bphase["encode_ms"] + bphase["sort_ms"],
+                  **bphase, "sort_passes": phase[-1]["sort_passes"], "reps": len(build_ms)},
+        "e2e": {"value": world * n / (e2e_ms / 1e3) / 1e9, "unit": "Gcells/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": N * 16, "d2h_bytes_per_step": M * W * 32},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    })
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_native(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,977 @@
+// api.cu -- the C ABI (include/dvl.h): argument validation, context state, device memory,
+// stream ordering and per-phase CUDA-event timing.  Every compute step is a kernel from
+// hilbert.cu / sort.cu / build.cu / update.cu; this file only orchestrates them.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dvl_common.cuh"
+#include "dvl_internal.h"
+
+using namespace dvl;
+
+namespace {
+
+enum Phase { PH_INGEST, PH_ENCODE, PH_SORT, PH_GATHER, PH_MAXV, PH_WSCAN, PH_BREDUCE, PH_EPI, PH_N };
+
+struct Dataset {
+  int64_t n = 0, n_pad = 0;
+  int M = 0, b = 0, Lmax = 0, key_bytes = 4, passes = 0, items = 16, tiles = 0;
+  uint32_t E = 0;
+  void* keys = nullptr;                 // sorted codes (n x key_bytes)
+  uint32_t* perm = nullptr;             // input id of each sorted cell
+  uint8_t* level_s = nullptr;           // n_pad
+  float* scal_s = nullptr;              // M x n_pad
+  std::vector<float> vmin, vmax;        // member data ranges (finite values)
+  // per-dataset update state
+  float* d_vmin = nullptr;              // M
+  float* d_vmax = nullptr;
+  float* d_lo = nullptr;                // M
+  float* d_inv = nullptr;
+  float4* d_rgba = nullptr;             // M x N
+  float2* d_tab = nullptr;              // M x N
+  unsigned long long* status1 = nullptr;  // tiles
+  unsigned long long* tile_prefix = nullptr;
+};
+
+}  // namespace
+
+struct dvl_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  dvl_alloc_fn alloc = nullptr;
+  dvl_free_fn free = nullptr;
+  void* user = nullptr;
+  uint32_t flags = 0;
+  std::string err;
+  std::unordered_map<void*, size_t> live;
+  size_t bytes = 0;
+
+  bool built = false;
+  Dataset ds;
+  std::vector<float> lo_h, hi_h, inv_h;  // domains
+  int N = 256;
+  float P = 1.0f, eps = 0.025f;
+  int mode = DVL_MAXV_CONSERVATIVE;
+  int shift = 0;
+
+  // small persistent device state
+  float* d_maxv = nullptr;
+  unsigned long long* d_qtot = nullptr;
+  uint32_t* d_ctr1 = nullptr;
+  uint32_t* d_err = nullptr;
+  float* d_stage = nullptr;          // N x 4 floats (one TF)
+  float* h_stage = nullptr;          // pinned
+  cudaEvent_t stage_ev = nullptr;
+  uint16_t* d_t1 = nullptr;
+  uint16_t* d_t2 = nullptr;
+  int nstates = 0;
+
+  // accumulators / outputs
+  uint32_t accW = 0;
+  int accM = 0;
+  Acc acc{};
+  dvl_vertex* d_out = nullptr;
+  unsigned long long* d_bin_lo = nullptr;
+  unsigned long long* d_bin_hi = nullptr;
+  uint32_t last_W = 0;
+
+  cudaEvent_t ev[PH_N][2] = {};
+  bool ev_used[PH_N] = {};
+  int sort_passes = 0;
+  int launches = 0;
+};
+
+namespace {
+
+struct Fail {
+  dvl_status s;
+};
+
+void set_err(dvl_ctx* c, const std::string& m) {
+  if (c) c->err = m;
+}
+
+#define CK(expr)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      set_err(ctx, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+      throw Fail{DVL_E_CUDA};                                                        \
+    }                                                                                \
+  } while (0)
+
+#define CKLAUNCH()                                                                   \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess) {                                                         \
+      set_err(ctx, std::string("kernel launch: ") + cudaGetErrorString(_e));         \
+      throw Fail{DVL_E_CUDA};                                                        \
+    }                                                                                \
+    ++ctx->launches;                                                                 \
+  } while (0)
+
+[[noreturn]] void fail(dvl_ctx* ctx, dvl_status s, const std::string& m) {
+  set_err(ctx, m);
+  throw Fail{s};
+}
+
+void* dmalloc(dvl_ctx* ctx, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~(size_t)255;
+  void* p = nullptr;
+  if (ctx->alloc) {
+    p = ctx->alloc(bytes, (void*)ctx->stream, ctx->user);
+    if (!p) fail(ctx, DVL_E_NOMEM, "device allocation of " + std::to_string(bytes) + " B failed");
+  } else {
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(ctx, DVL_E_NOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+  }
+  ctx->live[p] = bytes;
+  ctx->bytes += bytes;
+  return p;
+}
+
+template <typename T>
+T* dalloc(dvl_ctx* ctx, size_t count) {
+  return static_cast<T*>(dmalloc(ctx, count * sizeof(T)));
+}
+
+void dfree(dvl_ctx* ctx, void* p) {
+  if (!p) return;
+  auto it = ctx->live.find(p);
+  size_t bytes = it == ctx->live.end() ? 0 : it->second;
+  if (it != ctx->live.end()) {
+    ctx->live.erase(it);
+    ctx->bytes -= bytes;
+  }
+  if (ctx->free)
+    ctx->free(p, bytes, (void*)ctx->stream, ctx->user);
+  else
+    cudaFree(p);
+}
+
+void free_dataset(dvl_ctx* ctx, Dataset& d) {
+  void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
+                d.d_rgba, d.d_tab, d.status1, d.tile_prefix};
+  for (void* p : ps) dfree(ctx, p);
+  d = Dataset();
+}
+
+void tic(dvl_ctx* ctx, Phase ph) {
+  if (!(ctx->flags & DVL_FLAG_TIMING)) return;
+  cudaEventRecord(ctx->ev[ph][0], ctx->stream);
+}
+
+void toc(dvl_ctx* ctx, Phase ph) {
+  if (!(ctx->flags & DVL_FLAG_TIMING)) return;
+  cudaEventRecord(ctx->ev[ph][1], ctx->stream);
+  ctx->ev_used[ph] = true;
+}
+
+int ceil_log2_u64(uint64_t n) {
+  int c = 0;
+  while (c < 63 && (1ull << c) < n) ++c;
+  return c;
+}
+
+int ceil_lmax_p(int Lmax, float P) { return (int)std::ceil((double)Lmax * (double)P); }
+
+PowParams pow_params(float P) {
+  PowParams pw{};
+  if (P == 0.0f) {
+    pw.kind = kPow0;
+  } else if (P == 1.0f) {
+    pw.kind = kPow1;
+  } else if (P == std::floor(P) && P >= 2.0f && P <= 8.0f) {
+    pw.kind = kPowInt;
+    pw.k = (int)P;
+  } else {
+    pw.kind = kPowDet;
+  }
+  pw.P = P;
+  return pw;
+}
+
+int items_for(int M) {
+  if (M <= 4) return 16;
+  if (M <= 8) return 8;
+  if (M <= 16) return 4;
+  if (M <= 32) return 2;
+  return 1;
+}
+
+bool smem_tab_ok(const dvl_ctx* ctx) {
+  return (size_t)ctx->ds.M * ctx->N * sizeof(float2) <= 64 * 1024;
+}
+
+UpdParams upd_params(dvl_ctx* ctx) {
+  UpdParams p{};
+  const Dataset& d = ctx->ds;
+  p.n = d.n;
+  p.n_pad = d.n_pad;
+  p.M = d.M;
+  p.N = ctx->N;
+  p.level = d.level_s;
+  p.scal = d.scal_s;
+  p.lo = d.d_lo;
+  p.inv = d.d_inv;
+  p.tab = d.d_tab;
+  p.maxv = ctx->d_maxv;
+  p.eps = ctx->eps;
+  p.pw = pow_params(ctx->P);
+  p.scale = pow2f(ctx->shift);
+  p.offset = 0;
+  return p;
+}
+
+// O11: s = 61 - ceil(log2 n) - ceil(Lmax P)
+int compute_shift(dvl_ctx* ctx) {
+  return 61 - ceil_log2_u64((uint64_t)ctx->ds.n) - ceil_lmax_p(ctx->ds.Lmax, ctx->P);
+}
+
+void upload_domains(dvl_ctx* ctx) {
+  const int M = ctx->ds.M;
+  CK(cudaMemcpyAsync(ctx->ds.d_lo, ctx->lo_h.data(), sizeof(float) * M, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->ds.d_inv, ctx->inv_h.data(), sizeof(float) * M,
+                     cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// Copy one N x 4 TF from host memory into the device staging buffer (through pinned memory).
+void stage_tf(dvl_ctx* ctx, const float* rgba, int N) {
+  CK(cudaEventSynchronize(ctx->stage_ev));
+  memcpy(ctx->h_stage, rgba, sizeof(float) * 4 * N);
+  CK(cudaMemcpyAsync(ctx->d_stage, ctx->h_stage, sizeof(float) * 4 * N, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
+}
+
+// U0-U2: maxV, then pass 1 (weights + decoupled look-back scan).
+void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out) {
+  Dataset& d = ctx->ds;
+  ctx->shift = compute_shift(ctx);
+  UpdParams p = upd_params(ctx);
+  tic(ctx, PH_MAXV);
+  if (ctx->mode == DVL_MAXV_EXACT) {
+    int grid = (int)(d.n_pad / ((int64_t)kBlock * d.items));
+    launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);
+  } else {
+    launch_maxv_approx(ctx->mode, d.M, ctx->N, d.d_tab, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
+                       ctx->d_maxv, ctx->stream);
+  }
+  CKLAUNCH();
+  toc(ctx, PH_MAXV);
+  tic(ctx, PH_WSCAN);
+  CK(cudaMemsetAsync(d.status1, 0, sizeof(unsigned long long) * d.tiles, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_ctr1, 0, sizeof(uint32_t), ctx->stream));
+  launch_weights_scan(d.items, smem_tab_ok(ctx), export_q, p, d.status1, ctx->d_ctr1,
+                      d.tile_prefix, ctx->d_qtot, q_out, d.tiles, ctx->stream);
+  CKLAUNCH();
+  toc(ctx, PH_WSCAN);
+}
+
+void ensure_acc(dvl_ctx* ctx, uint32_t W) {
+  const int M = ctx->ds.M;
+  if (ctx->accW >= W && ctx->accM == M) return;
+  uint32_t cap = std::max(W, ctx->accW);
+  if (ctx->accM != M) cap = W;
+  Acc a{};
+  a.lo = dalloc<unsigned long long>(ctx, cap);
+  a.hi = dalloc<unsigned long long>(ctx, cap);
+  a.tmin = dalloc<uint32_t>(ctx, (size_t)cap * M);
+  a.tmax = dalloc<uint32_t>(ctx, (size_t)cap * M);
+  a.slo = dalloc<unsigned long long>(ctx, (size_t)cap * M);
+  a.shi = dalloc<unsigned long long>(ctx, (size_t)cap * M);
+  dvl_vertex* out = dalloc<dvl_vertex>(ctx, (size_t)cap * M);
+  unsigned long long* blo = dalloc<unsigned long long>(ctx, cap);
+  unsigned long long* bhi = dalloc<unsigned long long>(ctx, cap);
+  dfree(ctx, ctx->acc.lo);
+  dfree(ctx, ctx->acc.hi);
+  dfree(ctx, ctx->acc.tmin);
+  dfree(ctx, ctx->acc.tmax);
+  dfree(ctx, ctx->acc.slo);
+  dfree(ctx, ctx->acc.shi);
+  dfree(ctx, ctx->d_out);
+  dfree(ctx, ctx->d_bin_lo);
+  dfree(ctx, ctx->d_bin_hi);
+  ctx->acc = a;
+  ctx->d_out = out;
+  ctx->d_bin_lo = blo;
+  ctx->d_bin_hi = bhi;
+  ctx->accW = cap;
+  ctx->accM = M;
+  ctx->last_W = 0;
+  // identity of every accumulator plane (the epilogue restores it after each use);
+  // planes are laid out with the capacity as member stride, so init the whole capacity
+  launch_acc_init(a, cap, M, ctx->stream);
+  CKLAUNCH();
+}
+
+void identity_tf_host(std::vector<float>& tf, int N) {
+  tf.resize((size_t)N * 4);
+  for (int i = 0; i < N; ++i) {
+    float a = (float)((double)i / (double)(N - 1));
+    tf[4 * i] = tf[4 * i + 1] = tf[4 * i + 2] = 0.5f;
+    tf[4 * i + 3] = a;
+  }
+}
+
+void set_all_tfs(dvl_ctx* ctx, const std::vector<float>& tf, int N) {
+  for (int m = 0; m < ctx->ds.M; ++m) {
+    stage_tf(ctx, tf.data(), N);
+    launch_tf_prepare(ctx->d_stage, N, ctx->ds.d_rgba + (size_t)m * N, ctx->ds.d_tab + (size_t)m * N,
+                      ctx->stream);
+    CKLAUNCH();
+  }
+}
+
+bool maybe_degenerate(const dvl_ctx* ctx) {
+  if (ctx->eps <= 0.0f) return true;
+  // smallest possible weight: V = 0 -> r = eps, L = 0 -> f = eps^P (approximately)
+  double fmin = std::pow((double)ctx->eps, (double)ctx->P);
+  return fmin * std::ldexp(1.0, ctx->shift) < 4.0;
+}
+
+}  // namespace
+
+// ============================================================================== C ABI
+extern "C" {
+
+const char* dvl_status_string(dvl_status s) {
+  switch (s) {
+    case DVL_OK: return "DVL_OK";
+    case DVL_E_INVAL: return "DVL_E_INVAL";
+    case DVL_E_STATE: return "DVL_E_STATE";
+    case DVL_E_RANGE: return "DVL_E_RANGE";
+    case DVL_E_OVERLAP: return "DVL_E_OVERLAP";
+    case DVL_E_DEGENERATE: return "DVL_E_DEGENERATE";
+    case DVL_E_NOMEM: return "DVL_E_NOMEM";
+    case DVL_E_CUDA: return "DVL_E_CUDA";
+    case DVL_E_NCCL: return "DVL_E_NCCL";
+  }
+  return "DVL_E_UNKNOWN";
+}
+
+const char* dvl_last_error(const dvl_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void* dvl_stream(dvl_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int dvl_hilbert_states(void) { return hilbert_num_states(); }
+
+dvl_status dvl_hilbert_encode_host(uint64_t n, const uint32_t* xyz, int bits, uint64_t* codes) {
+  if ((n && (!xyz || !codes)) || bits < 1 || bits > 21) return DVL_E_INVAL;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    if ((x | y | z) >> bits) return DVL_E_INVAL;
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    codes[i] = hilbert_encode_host(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], bits);
+  return DVL_OK;
+}
+
+dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
+  if (!init || !out) return DVL_E_INVAL;
+  *out = nullptr;
+  dvl_ctx* ctx = new dvl_ctx();
+  try {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (init->device < 0 || init->device >= ndev) fail(ctx, DVL_E_INVAL, "bad device ordinal");
+    if ((init->alloc == nullptr) != (init->free == nullptr))
+      fail(ctx, DVL_E_INVAL, "alloc and free must both be set or both be NULL");
+    ctx->device = init->device;
+    ctx->alloc = init->alloc;
+    ctx->free = init->free;
+    ctx->user = init->user;
+    ctx->flags = init->flags;
+    CK(cudaSetDevice(ctx->device));
+    if (init->cuda_stream) {
+      ctx->stream = (cudaStream_t)init->cuda_stream;
+    } else {
+      CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    static bool prepared = false;
+    if (!prepared) {
+      CK(prepare_onesweep());
+      CK(prepare_update_kernels());
+      prepared = true;
+    }
+    ctx->d_maxv = dalloc<float>(ctx, 1);
+    ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
+    ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
+    ctx->d_err = dalloc<uint32_t>(ctx, 1);
+    ctx->d_stage = dalloc<float>(ctx, 4 * kMaxN);
+    CK(cudaMallocHost(&ctx->h_stage, sizeof(float) * 4 * kMaxN));
+    CK(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
+    for (int i = 0; i < PH_N; ++i) {
+      CK(cudaEventCreate(&ctx->ev[i][0]));
+      CK(cudaEventCreate(&ctx->ev[i][1]));
+    }
+    std::vector<uint16_t> t1, t2;
+    hilbert_tables_host(&t1, &t2, &ctx->nstates);
+    ctx->d_t1 = dalloc<uint16_t>(ctx, t1.size());
+    ctx->d_t2 = dalloc<uint16_t>(ctx, t2.size());
+    CK(cudaMemcpyAsync(ctx->d_t1, t1.data(), t1.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_t2, t2.data(), t2.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    // keep the message visible through a process-wide fallback
+    fprintf(stderr, "dvl_create: %s\n", ctx->err.c_str());
+    dvl_destroy(ctx);
+    return f.s;
+  }
+  *out = ctx;
+  return DVL_OK;
+}
+
+void dvl_destroy(dvl_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_dataset(ctx, ctx->ds);
+  std::vector<void*> ps;
+  for (auto& kv : ctx->live) ps.push_back(kv.first);
+  for (void* p : ps) dfree(ctx, p);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->stage_ev) cudaEventDestroy(ctx->stage_ev);
+  for (int i = 0; i < PH_N; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (ctx->ev[i][j]) cudaEventDestroy(ctx->ev[i][j]);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const uint8_t* level,
+                     uint32_t members, const float* const* scalars, dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  ctx->err.clear();
+  ctx->launches = 0;
+  Dataset d;
+  std::vector<void*> tmp;   // temporaries freed on every exit
+  auto cleanup = [&]() {
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (void* p : tmp) dfree(ctx, p);
+  };
+  try {
+    if (n == 0) fail(ctx, DVL_E_INVAL, "n must be >= 1");
+    if (n >= (1ull << 30)) fail(ctx, DVL_E_RANGE, "n must be < 2^30 per device");
+    if (members < 1 || members > (uint32_t)kMaxM) fail(ctx, DVL_E_INVAL, "members must be in [1, 64]");
+    if (!lower_xyz || !level || !scalars) fail(ctx, DVL_E_INVAL, "NULL input pointer");
+    for (uint32_t m = 0; m < members; ++m)
+      if (!scalars[m]) fail(ctx, DVL_E_INVAL, "NULL scalar pointer");
+    if (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE) fail(ctx, DVL_E_INVAL, "bad dvl_mem");
+    CK(cudaSetDevice(ctx->device));
+    const int M = (int)members;
+    const int64_t nn = (int64_t)n;
+    cudaStream_t st = ctx->stream;
+
+    // ---- stage inputs on the device
+    const uint32_t* d_lower = lower_xyz;
+    const uint8_t* d_level = level;
+    std::vector<const float*> scal_ptrs(scalars, scalars + M);
+    tic(ctx, PH_INGEST);
+    if (where == DVL_MEM_HOST) {
+      uint32_t* l = dalloc<uint32_t>(ctx, 3 * (size_t)nn);
+      tmp.push_back(l);
+      uint8_t* lv = dalloc<uint8_t>(ctx, nn);
+      tmp.push_back(lv);
+      float* sc = dalloc<float>(ctx, (size_t)M * nn);
+      tmp.push_back(sc);
+      CK(cudaMemcpyAsync(l, lower_xyz, 12 * (size_t)nn, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(lv, level, nn, cudaMemcpyHostToDevice, st));
+      for (int m = 0; m < M; ++m) {
+        CK(cudaMemcpyAsync(sc + (size_t)m * nn, scalars[m], 4 * (size_t)nn, cudaMemcpyHostToDevice, st));
+        scal_ptrs[m] = sc + (size_t)m * nn;
+      }
+      d_lower = l;
+      d_level = lv;
+    }
+    const float** d_ptrs = (const float**)dmalloc(ctx, sizeof(float*) * M);
+    tmp.push_back((void*)d_ptrs);
+    CK(cudaMemcpyAsync(d_ptrs, scal_ptrs.data(), sizeof(float*) * M, cudaMemcpyHostToDevice, st));
+
+    // ---- B0: ingest reduction
+    IngestOut h_ing;
+    memset(&h_ing, 0, sizeof h_ing);
+    for (int m = 0; m < 64; ++m) h_ing.vmin[m] = 0xffffffffu;
+    IngestOut* d_ing = (IngestOut*)dmalloc(ctx, sizeof(IngestOut));
+    tmp.push_back(d_ing);
+    CK(cudaMemcpyAsync(d_ing, &h_ing, sizeof h_ing, cudaMemcpyHostToDevice, st));
+    int grid = (int)std::min<int64_t>((nn + kBlock - 1) / kBlock, 148 * 8);
+    launch_ingest(d_lower, d_level, d_ptrs, nn, M, d_ing, grid, st);
+    CKLAUNCH();
+    toc(ctx, PH_INGEST);
+    CK(cudaMemcpyAsync(&h_ing, d_ing, sizeof h_ing, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_ing.err & kErrInval) fail(ctx, DVL_E_INVAL, "a cell has L > 20 or a lower corner not a multiple of 2^L");
+    if (h_ing.extent > (1ull << 21)) fail(ctx, DVL_E_RANGE, "logical extent E > 2^21");
+    if (ceil_lmax_p((int)h_ing.lmax, ctx->P) > 100)
+      fail(ctx, DVL_E_RANGE, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
+    d.n = nn;
+    d.M = M;
+    d.E = (uint32_t)h_ing.extent;
+    d.b = std::max(1, ceil_log2_u64(h_ing.extent));
+    d.Lmax = (int)h_ing.lmax;
+    d.key_bytes = 3 * d.b <= 32 ? 4 : 8;
+    d.passes = (3 * d.b + 7) / 8;
+    d.items = items_for(M);
+    const int64_t T = (int64_t)kBlock * d.items;
+    d.tiles = (int)((nn + T - 1) / T);
+    d.n_pad = (int64_t)d.tiles * T;
+    d.vmin.resize(M);
+    d.vmax.resize(M);
+    for (int m = 0; m < M; ++m) {
+      d.vmin[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmin[m]) : 0.0f;
+      d.vmax[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmax[m]) : 0.0f;
+    }
+
+    // ---- B1: Hilbert encode + digit histograms
+    const int kb = d.key_bytes;
+    void* kA = dmalloc(ctx, (size_t)kb * nn);
+    void* kB = dmalloc(ctx, (size_t)kb * nn);
+    uint32_t* iA = dalloc<uint32_t>(ctx, nn);
+    uint32_t* iB = dalloc<uint32_t>(ctx, nn);
+    uint32_t* hist = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
+    uint32_t* base = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
+    const int64_t stiles = (nn + kSortTile - 1) / kSortTile;
+    uint32_t* status = dalloc<uint32_t>(ctx, (size_t)d.passes * stiles * 256);
+    uint32_t* ctrs = dalloc<uint32_t>(ctx, d.passes);
+    tmp.push_back(hist);
+    tmp.push_back(base);
+    tmp.push_back(status);
+    tmp.push_back(ctrs);
+    CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * d.passes * 256, st));
+    CK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * d.passes * stiles * 256, st));
+    CK(cudaMemsetAsync(ctrs, 0, sizeof(uint32_t) * d.passes, st));
+    tic(ctx, PH_ENCODE);
+    launch_encode_hist(d_lower, d_level, nn, d.b, kb, d.passes, ctx->d_t1, ctx->d_t2,
+                       ctx->nstates, kA, iA, hist, grid, st);
+    CKLAUNCH();
+    toc(ctx, PH_ENCODE);
+
+    // ---- B2: onesweep passes (a pass whose digit is constant is the identity: skipped)
+    tic(ctx, PH_SORT);
+    launch_hist_scan(hist, base, d.passes, st);
+    CKLAUNCH();
+    std::vector<uint32_t> h_hist((size_t)d.passes * 256);
+    CK(cudaMemcpyAsync(h_hist.data(), hist, 4 * h_hist.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    void* kin = kA;
+    void* kout = kB;
+    uint32_t* vin = iA;
+    uint32_t* vout = iB;
+    int done = 0;
+    for (int p = 0; p < d.passes; ++p) {
+      uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
+      if ((int64_t)mx == nn) continue;
+      launch_onesweep(kin, vin, kout, vout, nn, kb, 8 * p, base + p * 256,
+                      status + (size_t)p * stiles * 256, ctrs + p, st);
+      CKLAUNCH();
+      std::swap(kin, kout);
+      std::swap(vin, vout);
+      ++done;
+    }
+    ctx->sort_passes = done;
+    toc(ctx, PH_SORT);
+    d.keys = kin;
+    d.perm = vin;
+    tmp.push_back(kout);
+    tmp.push_back(vout);
+
+    // ---- B3: permute into curve order + overlap validation
+    d.level_s = dalloc<uint8_t>(ctx, d.n_pad);
+    d.scal_s = dalloc<float>(ctx, (size_t)M * d.n_pad);
+    CK(cudaMemsetAsync(d.level_s, 0, d.n_pad, st));
+    CK(cudaMemsetAsync(d.scal_s, 0, sizeof(float) * M * d.n_pad, st));
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
+    tic(ctx, PH_GATHER);
+    launch_gather_validate(d.keys, kb, d.perm, d_level, d_ptrs, nn, M, d.n_pad, d.level_s,
+                           d.scal_s, ctx->d_err, grid, st);
+    CKLAUNCH();
+    toc(ctx, PH_GATHER);
+    uint32_t herr = 0;
+    CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (herr & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
+
+    // ---- per-dataset update state
+    d.d_vmin = dalloc<float>(ctx, M);
+    d.d_vmax = dalloc<float>(ctx, M);
+    d.d_lo = dalloc<float>(ctx, M);
+    d.d_inv = dalloc<float>(ctx, M);
+    d.d_rgba = dalloc<float4>(ctx, (size_t)M * kMaxN);
+    d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
+    d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
+    d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
+    CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
+  } catch (Fail& f) {
+    cleanup();
+    free_dataset(ctx, d);
+    return f.s;
+  }
+  cleanup();
+  // commit: replace the old dataset
+  free_dataset(ctx, ctx->ds);
+  ctx->ds = d;
+  ctx->built = true;
+  ctx->N = 256;
+  ctx->lo_h = ctx->ds.vmin;
+  ctx->hi_h = ctx->ds.vmax;
+  ctx->inv_h.resize(ctx->ds.M);
+  for (int m = 0; m < ctx->ds.M; ++m) {
+    float lo = ctx->lo_h[m], hi = ctx->hi_h[m];
+    ctx->inv_h[m] = hi > lo ? 1.0f / (hi - lo) : 0.0f;
+  }
+  if (ctx->accM != ctx->ds.M) ctx->accW = 0;
+  ctx->last_W = 0;
+  try {
+    upload_domains(ctx);
+    std::vector<float> tf;
+    identity_tf_host(tf, ctx->N);
+    set_all_tfs(ctx, tf, ctx->N);
+    run_weights(ctx, false, nullptr);
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    ctx->built = false;
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_set_params(dvl_ctx* ctx, float P, float eps, dvl_maxv_mode mode) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!(P >= 0.0f && P <= 16.0f)) {
+    set_err(ctx, "P must be in [0, 16]");
+    return DVL_E_INVAL;
+  }
+  if (!(eps >= 0.0f && eps <= 1.0f)) {
+    set_err(ctx, "eps must be in [0, 1]");
+    return DVL_E_INVAL;
+  }
+  if (mode != DVL_MAXV_CONSERVATIVE && mode != DVL_MAXV_PER_ENTRY && mode != DVL_MAXV_EXACT) {
+    set_err(ctx, "bad maxV mode");
+    return DVL_E_INVAL;
+  }
+  if (ctx->built && ceil_lmax_p(ctx->ds.Lmax, P) > 100) {
+    set_err(ctx, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
+    return DVL_E_RANGE;
+  }
+  ctx->P = P;
+  ctx->eps = eps;
+  ctx->mode = mode;
+  if (ctx->built) {
+    try {
+      CK(cudaSetDevice(ctx->device));
+      run_weights(ctx, false, nullptr);
+    } catch (Fail& f) {
+      return f.s;
+    }
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_set_domain(dvl_ctx* ctx, uint32_t member, float lo, float hi) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_set_domain before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (member >= (uint32_t)ctx->ds.M || !std::isfinite(lo) || !std::isfinite(hi) || hi < lo) {
+    set_err(ctx, "bad member or domain");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    ctx->lo_h[member] = lo;
+    ctx->hi_h[member] = hi;
+    ctx->inv_h[member] = hi > lo ? 1.0f / (hi - lo) : 0.0f;
+    CK(cudaStreamSynchronize(ctx->stream));   // host vectors are the copy source
+    upload_domains(ctx);
+    run_weights(ctx, false, nullptr);
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+static dvl_status check_tf(dvl_ctx* ctx, const float* rgba, uint32_t N) {
+  if (!rgba || N < 2 || N > (uint32_t)kMaxN) {
+    set_err(ctx, "TF size N must be in [2, 4096]");
+    return DVL_E_INVAL;
+  }
+  for (uint32_t i = 0; i < 4 * N; ++i)
+    if (!(rgba[i] >= 0.0f && rgba[i] <= 1.0f)) {
+      set_err(ctx, "TF channels must be in [0, 1]");
+      return DVL_E_INVAL;
+    }
+  return DVL_OK;
+}
+
+dvl_status dvl_update_tf(dvl_ctx* ctx, uint32_t member, const float* rgba, uint32_t N) {
+  if (!ctx) return DVL_E_INVAL;
+  ctx->launches = 0;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_update_tf before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (member >= (uint32_t)ctx->ds.M) {
+    set_err(ctx, "member out of range");
+    return DVL_E_INVAL;
+  }
+  dvl_status s = check_tf(ctx, rgba, N);
+  if (s != DVL_OK) return s;
+  if ((int)N != ctx->N) {
+    set_err(ctx, "all members share one TF size; use dvl_reset_tfs to change it");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    stage_tf(ctx, rgba, (int)N);
+    launch_tf_prepare(ctx->d_stage, (int)N, ctx->ds.d_rgba + (size_t)member * N,
+                      ctx->ds.d_tab + (size_t)member * N, ctx->stream);
+    CKLAUNCH();
+    run_weights(ctx, false, nullptr);
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_reset_tfs(dvl_ctx* ctx, uint32_t N) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_reset_tfs before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (N < 2 || N > (uint32_t)kMaxN) {
+    set_err(ctx, "TF size N must be in [2, 4096]");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    ctx->N = (int)N;
+    std::vector<float> tf;
+    identity_tf_host(tf, (int)N);
+    set_all_tfs(ctx, tf, (int)N);
+    run_weights(ctx, false, nullptr);
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  ctx->launches = 0;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_get_polylines before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (W < 2 || W > kMaxW || !out || (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE)) {
+    set_err(ctx, "W must be in [2, 65536] and out non-NULL");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    ensure_acc(ctx, W);
+    Dataset& d = ctx->ds;
+    UpdParams p = upd_params(ctx);
+    // the member planes are indexed m * W + x for this call (capacity >= W); the epilogue
+    // restores the identity of every entry it reads, so all entries stay identity
+    Acc a = ctx->acc;
+    tic(ctx, PH_BREDUCE);
+    launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a, ctx->d_err,
+                      d.tiles, ctx->stream);
+    CKLAUNCH();
+    toc(ctx, PH_BREDUCE);
+    dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
+    tic(ctx, PH_EPI);
+    launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
+    CKLAUNCH();
+    toc(ctx, PH_EPI);
+    ctx->last_W = W;
+    if (where == DVL_MEM_HOST) {
+      CK(cudaMemcpyAsync(out, ctx->d_out, sizeof(dvl_vertex) * (size_t)W * d.M,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (where == DVL_MEM_HOST || maybe_degenerate(ctx)) {
+      uint32_t herr = 0;
+      CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (herr & kErrDegenerate) {
+        CK(cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
+        ctx->last_W = 0;
+        fail(ctx, DVL_E_DEGENERATE, "all weights are 0 (Qtot = 0)");
+      }
+    }
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_info(dvl_ctx* ctx, dvl_info_t* info) {
+  if (!ctx || !info) return DVL_E_INVAL;
+  memset(info, 0, sizeof *info);
+  try {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    info->P = ctx->P;
+    info->eps = ctx->eps;
+    info->maxv_mode = ctx->mode;
+    info->device_bytes = ctx->bytes;
+    info->tf_size = ctx->N;
+    if (ctx->built) {
+      const Dataset& d = ctx->ds;
+      info->n = (uint64_t)d.n;
+      info->members = (uint32_t)d.M;
+      info->extent = d.E;
+      info->bits = d.b;
+      info->Lmax = d.Lmax;
+      info->key_bytes = d.key_bytes;
+      info->shift = ctx->shift;
+      info->cells_per_tile = kBlock * d.items;
+      CK(cudaMemcpy(&info->maxV, ctx->d_maxv, 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&info->Qtot, ctx->d_qtot, 8, cudaMemcpyDeviceToHost));
+    }
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+static cudaMemcpyKind out_kind(dvl_mem where) {
+  return where == DVL_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+}
+
+dvl_status dvl_get_sorted(dvl_ctx* ctx, uint64_t* codes, uint64_t* ids, dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "no dataset");
+    return DVL_E_STATE;
+  }
+  std::vector<void*> tmp;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->ds.n;
+    uint64_t* dc = nullptr;
+    uint64_t* di = nullptr;
+    if (codes) {
+      dc = where == DVL_MEM_DEVICE ? codes : dalloc<uint64_t>(ctx, n);
+      if (where != DVL_MEM_DEVICE) tmp.push_back(dc);
+    }
+    if (ids) {
+      di = where == DVL_MEM_DEVICE ? ids : dalloc<uint64_t>(ctx, n);
+      if (where != DVL_MEM_DEVICE) tmp.push_back(di);
+    }
+    launch_widen(ctx->ds.keys, ctx->ds.key_bytes, ctx->ds.perm, n, dc, di, ctx->stream);
+    CKLAUNCH();
+    if (where == DVL_MEM_HOST) {
+      if (codes) CK(cudaMemcpyAsync(codes, dc, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+      if (ids) CK(cudaMemcpyAsync(ids, di, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    for (void* p : tmp) dfree(ctx, p);
+    return f.s;
+  }
+  for (void* p : tmp) dfree(ctx, p);
+  return DVL_OK;
+}
+
+dvl_status dvl_get_sorted_data(dvl_ctx* ctx, uint8_t* level_sorted, float* scalars_sorted,
+                               dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "no dataset");
+    return DVL_E_STATE;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const Dataset& d = ctx->ds;
+    if (level_sorted)
+      CK(cudaMemcpyAsync(level_sorted, d.level_s, d.n, out_kind(where), ctx->stream));
+    if (scalars_sorted)
+      CK(cudaMemcpy2DAsync(scalars_sorted, 4 * d.n, d.scal_s, 4 * d.n_pad, 4 * d.n, d.M,
+                           out_kind(where), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_get_prefix(dvl_ctx* ctx, uint64_t* Q, dvl_mem where) {
+  if (!ctx || !Q) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "no dataset");
+    return DVL_E_STATE;
+  }
+  void* tmp = nullptr;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = ctx->ds.n;
+    unsigned long long* dq =
+        where == DVL_MEM_DEVICE ? (unsigned long long*)Q : dalloc<unsigned long long>(ctx, n);
+    if (where != DVL_MEM_DEVICE) tmp = dq;
+    run_weights(ctx, true, dq);
+    if (where == DVL_MEM_HOST) CK(cudaMemcpyAsync(Q, dq, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    dfree(ctx, tmp);
+    return f.s;
+  }
+  dfree(ctx, tmp);
+  return DVL_OK;
+}
+
+dvl_status dvl_get_bin_ranges(dvl_ctx* ctx, uint32_t W, uint64_t* lo, uint64_t* hi,
+                              dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built || ctx->last_W != W || W == 0) {
+    set_err(ctx, "no polylines of this width yet");
+    return DVL_E_STATE;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    if (lo) CK(cudaMemcpyAsync(lo, ctx->d_bin_lo, 8 * (size_t)W, out_kind(where), ctx->stream));
+    if (hi) CK(cudaMemcpyAsync(hi, ctx->d_bin_hi, 8 * (size_t)W, out_kind(where), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
+  if (!ctx || !t) return DVL_E_INVAL;
+  memset(t, 0, sizeof *t);
+  try {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float* dst[PH_N] = {&t->ingest_ms, &t->encode_ms, &t->sort_ms, &t->gather_ms,
+                        &t->maxv_ms, &t->weights_scan_ms, &t->bin_reduce_ms, &t->epilogue_ms};
+    for (int i = 0; i < PH_N; ++i)
+      if (ctx->ev_used[i]) CK(cudaEventElapsedTime(dst[i], ctx->ev[i][0], ctx->ev[i][1]));
+    t->sort_passes = ctx->sort_passes;
+    t->launches = ctx->launches;
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+}  // extern "C"

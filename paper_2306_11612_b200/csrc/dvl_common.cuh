@@ -1,0 +1,242 @@
+// dvl_common.cuh -- shared definitions of the sm_100a DVL library (product side).
+//
+// Nothing in this directory is shared with oracle/: the fp32 recipes below are written
+// from DESIGN.md section 3 (readings O6-O11), with explicit round-to-nearest intrinsics
+// so that no contraction or fast-math can change a bit (the library is also compiled
+// with -fmad=false -ftz=false -prec-div=true).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dvl {
+
+constexpr int kBlock = 256;            // threads of every streaming kernel
+constexpr int kSortItems = 16;         // keys per thread in the onesweep passes
+constexpr int kSortTile = kBlock * kSortItems;
+constexpr int kMaxN = 4096;            // largest TF
+constexpr int kMaxM = 64;              // largest ensemble
+constexpr uint32_t kMaxW = 65536;      // largest plot width
+
+// status words of the weight scan's decoupled look-back (u64: 2 flag bits + 62 value bits)
+constexpr uint64_t kScanAgg = 1ull << 62;
+constexpr uint64_t kScanInc = 2ull << 62;
+constexpr uint64_t kScanMask = (1ull << 62) - 1;
+// status words of the onesweep digit look-back (u32: 2 flag bits + 30 count bits)
+constexpr uint32_t kSortAgg = 1u << 30;
+constexpr uint32_t kSortInc = 2u << 30;
+constexpr uint32_t kSortMask = (1u << 30) - 1;
+
+constexpr float kSumScale = 281474976710656.0f;   // 2^48: fixed point of per-thread t sums
+constexpr double kSumUnscale = 1.0 / 281474976710656.0;
+
+// error bits written by kernels
+constexpr uint32_t kErrInval = 1u;      // L > 20 or lower not a multiple of 2^L
+constexpr uint32_t kErrOverlap = 2u;    // codes not strictly increasing / dyadic overlap
+constexpr uint32_t kErrDegenerate = 4u; // Qtot == 0
+
+// exponent classes of Eq. 3's ^P (reading O10)
+enum PowKind : int { kPow0 = 0, kPow1 = 1, kPowInt = 2, kPowDet = 3 };
+
+struct PowParams {
+  int kind;
+  int k;       // integer exponent for kPowInt
+  float P;     // exponent for kPowDet
+};
+
+// Inputs of the two update passes.
+struct UpdParams {
+  int64_t n;               // cells on this device
+  int64_t n_pad;           // member stride of scal (multiple of the tile)
+  int M, N;
+  const uint8_t* level;    // n_pad, curve order
+  const float* scal;       // M x n_pad, curve order
+  const float* lo;         // M domain lower bounds
+  const float* inv;        // M inverse domain widths
+  const float2* tab;       // M x N (alpha[i], alpha[i+1]-alpha[i])
+  const float* maxv;       // device scalar
+  float eps;
+  PowParams pw;
+  float scale;             // 2^s
+  uint64_t offset;         // global prefix before this device's cells (sharding)
+};
+
+// Per-bin accumulators of U4 (integer-exact, combined with atomics in any order).
+struct Acc {
+  unsigned long long* lo;    // W: first cell (min)
+  unsigned long long* hi;    // W: last cell (max)
+  uint32_t* tmin;            // M x W: min of t bits (t >= 0, so bits order like values)
+  uint32_t* tmax;            // M x W
+  unsigned long long* slo;   // M x W: low word of the 128-bit sum of round(t_part * 2^48)
+  unsigned long long* shi;   // M x W: high word
+};
+
+// ------------------------------------------------------------------ fp32 recipes
+// 2^k as fp32, exact for -149 <= k <= 127.
+__host__ __device__ inline float pow2f(int k) {
+  uint32_t u = k >= -126 ? (uint32_t)(k + 127) << 23 : 1u << (k + 149);
+  float f;
+#ifdef __CUDA_ARCH__
+  f = __uint_as_float(u);
+#else
+  __builtin_memcpy(&f, &u, 4);
+#endif
+  return f;
+}
+
+// O7: t = clamp((v - lo) * inv, 0, 1), NaN -> 0.
+__device__ __forceinline__ float norm_t(float v, float lo, float inv) {
+  float x = __fmul_rn(__fsub_rn(v, lo), inv);
+  return x > 0.0f ? (x < 1.0f ? x : 1.0f) : 0.0f;
+}
+
+// O8: piecewise-linear lookup on t * (N - 1) with the slope table tab[i] =
+// (A[i], A[i+1] - A[i]) and tab[N-1] = (A[N-1], 0): at pos = N-1 the result is A[N-1].
+__device__ __forceinline__ float sample_tab(const float2* tab, float nm1, float t) {
+  float pos = __fmul_rn(t, nm1);
+  int i0 = (int)pos;
+  float fr = __fsub_rn(pos, (float)i0);
+  float2 e = tab[i0];
+  return __fmaf_rn(fr, e.y, e.x);
+}
+
+// O8 on an RGBA table (one channel c), identical op order.
+__device__ __forceinline__ float sample_rgba(const float4* tf, int N, float t, int c) {
+  float nm1 = (float)(N - 1);
+  float pos = __fmul_rn(t, nm1);
+  if (pos >= nm1) {
+    float4 e = tf[N - 1];
+    return c == 0 ? e.x : c == 1 ? e.y : c == 2 ? e.z : e.w;
+  }
+  int i0 = (int)pos;
+  float fr = __fsub_rn(pos, (float)i0);
+  float4 a = tf[i0], b = tf[i0 + 1];
+  float a0 = c == 0 ? a.x : c == 1 ? a.y : c == 2 ? a.z : a.w;
+  float a1 = c == 0 ? b.x : c == 1 ? b.y : c == 2 ? b.z : b.w;
+  return __fmaf_rn(fr, __fsub_rn(a1, a0), a0);
+}
+
+// O10 detpow for non-integer P: log2 by atanh series, exp2 by Taylor polynomial.
+__device__ __forceinline__ float det_log2(float g) {
+  int e;
+  float m = frexpf(g, &e);
+  if (m < 0x1.6a09e6p-1f) {
+    m = __fmul_rn(m, 2.0f);
+    e = e - 1;
+  }
+  float u = __fdiv_rn(__fsub_rn(m, 1.0f), __fadd_rn(m, 1.0f));
+  float z = __fmul_rn(u, u);
+  float p = 0x1.c71c72p-4f;
+  p = __fmaf_rn(p, z, 0x1.24924ap-3f);
+  p = __fmaf_rn(p, z, 0x1.99999ap-3f);
+  p = __fmaf_rn(p, z, 0x1.555556p-2f);
+  p = __fmaf_rn(p, z, 1.0f);
+  float t1 = __fmul_rn(u, p);
+  float t2 = __fmul_rn(t1, 0x1.715476p+1f);
+  return __fadd_rn((float)e, t2);
+}
+
+__device__ __forceinline__ float det_exp2(float y) {
+  float k = floorf(y);
+  float fr = __fsub_rn(y, k);
+  float w = __fmul_rn(fr, 0x1.62e430p-1f);
+  float p = 0x1.a01a02p-16f;
+  p = __fmaf_rn(p, w, 0x1.a01a02p-13f);
+  p = __fmaf_rn(p, w, 0x1.6c16c2p-10f);
+  p = __fmaf_rn(p, w, 0x1.111112p-7f);
+  p = __fmaf_rn(p, w, 0x1.555556p-5f);
+  p = __fmaf_rn(p, w, 0x1.555556p-3f);
+  p = __fmaf_rn(p, w, 0.5f);
+  p = __fmaf_rn(p, w, 1.0f);
+  p = __fmaf_rn(p, w, 1.0f);
+  if (k < -149.0f) return 0.0f;
+  if (k > 127.0f) return __int_as_float(0x7f800000);
+  return __fmul_rn(p, pow2f((int)k));
+}
+
+__device__ __forceinline__ float pow_p(float g, const PowParams& pw) {
+  if (pw.kind == kPow0) return 1.0f;
+  if (pw.kind == kPow1) return g;
+  if (pw.kind == kPowInt) {
+    float f = g;
+    for (int k = 1; k < pw.k; ++k) f = __fmul_rn(f, g);
+    return f;
+  }
+  if (g == 0.0f) return 0.0f;
+  return det_exp2(__fmul_rn(pw.P, det_log2(g)));
+}
+
+// Eq. 3 with the minimum importance clamped on the ratio (reading A9-A11).
+__device__ __forceinline__ float importance(float V, float maxv, int L, float eps,
+                                            const PowParams& pw) {
+  float r = maxv > 0.0f ? __fdiv_rn(V, maxv) : 0.0f;
+  r = r > eps ? r : eps;
+  r = r < 1.0f ? r : 1.0f;
+  float g = __fmul_rn(r, pow2f(L));
+  return pow_p(g, pw);
+}
+
+// ------------------------------------------------------------------ small helpers
+template <int ITEMS>
+__device__ __forceinline__ void load_f(const float* __restrict__ p, float (&v)[ITEMS]) {
+  if constexpr (ITEMS % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < ITEMS / 4; ++j) {
+      float4 q = __ldg(reinterpret_cast<const float4*>(p) + j);
+      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+  } else if constexpr (ITEMS == 2) {
+    float2 q = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) v[j] = __ldg(p + j);
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void load_u8(const uint8_t* __restrict__ p, int (&v)[ITEMS]) {
+  if constexpr (ITEMS == 16) {
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = (w[j >> 2] >> (8 * (j & 3))) & 0xff;
+  } else if constexpr (ITEMS == 8) {
+    uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+    uint32_t w[2] = {q.x, q.y};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (w[j >> 2] >> (8 * (j & 3))) & 0xff;
+  } else if constexpr (ITEMS == 4) {
+    uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(p));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = (w >> (8 * j)) & 0xff;
+  } else {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) v[j] = __ldg(p + j);
+  }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_incl_scan_u64(unsigned long long v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// 128-bit atomic add of a u64 into (lo, hi) words: exact in any order.
+__device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned long long* hi,
+                                                unsigned long long v) {
+  if (v == 0) return;
+  unsigned long long old = atomicAdd(lo, v);
+  if (old + v < old) atomicAdd(hi, 1ull);
+}
+
+}  // namespace dvl

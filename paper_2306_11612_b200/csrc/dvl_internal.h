@@ -1,0 +1,73 @@
+// dvl_internal.h -- host-side declarations shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "dvl.h"
+
+namespace dvl {
+
+struct UpdParams;
+struct Acc;
+
+// hilbert.cu
+int hilbert_num_states();
+uint64_t hilbert_encode_host(uint32_t x, uint32_t y, uint32_t z, int b);
+void hilbert_tables_host(std::vector<uint16_t>* t1, std::vector<uint16_t>* t2, int* nstates);
+void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, int b,
+                        int key_bytes, int passes, const uint16_t* d_t1, const uint16_t* d_t2,
+                        int nstates, void* keys, uint32_t* ids, uint32_t* hist, int grid,
+                        cudaStream_t st);
+
+// sort.cu
+cudaError_t prepare_onesweep();
+void launch_hist_scan(const uint32_t* hist, uint32_t* base, int passes, cudaStream_t st);
+void launch_onesweep(const void* kin, const uint32_t* vin, void* kout, uint32_t* vout, int64_t n,
+                     int key_bytes, int shift, const uint32_t* digit_base, uint32_t* status,
+                     uint32_t* tile_ctr, cudaStream_t st);
+
+// build.cu
+struct IngestOut {                 // device-side results of the ingest reduction
+  unsigned long long extent;      // max(lower + 2^L)
+  uint32_t lmax;
+  uint32_t err;
+  uint32_t vmin[64];              // ordered-int encoded floats (finite values only)
+  uint32_t vmax[64];
+  uint32_t any[64];               // 1 if the member has a finite value
+};
+void launch_ingest(const uint32_t* lower, const uint8_t* level, const float* const* scal,
+                   int64_t n, int M, IngestOut* out, int grid, cudaStream_t st);
+void launch_gather_validate(const void* keys, int key_bytes, const uint32_t* perm,
+                            const uint8_t* level_in, const float* const* scal_in, int64_t n,
+                            int M, int64_t n_pad, uint8_t* level_s, float* scal_s,
+                            uint32_t* err, int grid, cudaStream_t st);
+void launch_widen(const void* keys, int key_bytes, const uint32_t* perm, int64_t n,
+                  uint64_t* codes_out, uint64_t* ids_out, cudaStream_t st);
+float ordered_to_float(uint32_t u);
+
+// update.cu
+void launch_tf_prepare(const float* rgba_in, int N, float4* rgba_out, float2* tab_out,
+                       cudaStream_t st);
+void launch_maxv_approx(int mode, int M, int N, const float2* tab, const float* vmin,
+                        const float* vmax, const float* lo, const float* inv, float* maxv,
+                        cudaStream_t st);
+void launch_maxv_exact(const UpdParams& p, float* maxv, int grid, cudaStream_t st);
+void launch_weights_scan(int items, bool smem_tab, bool export_q, const UpdParams& p,
+                         unsigned long long* status, uint32_t* ctr,
+                         unsigned long long* tile_prefix, unsigned long long* qtot,
+                         unsigned long long* q_out, int tiles, cudaStream_t st);
+void launch_bin_reduce(int items, bool smem_tab, const UpdParams& p,
+                       const unsigned long long* tile_prefix, const unsigned long long* qtot,
+                       uint32_t W, const Acc& acc, uint32_t* err, int tiles, cudaStream_t st);
+void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
+                     dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
+                     cudaStream_t st);
+void launch_acc_init(const Acc& acc, uint32_t W, int M, cudaStream_t st);
+cudaError_t prepare_update_kernels();
+size_t bin_reduce_smem(int items, int M, int N, bool smem_tab);
+
+}  // namespace dvl

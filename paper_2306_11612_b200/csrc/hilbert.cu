@@ -1,0 +1,217 @@
+// hilbert.cu -- B1: centroid quantisation + 3D Hilbert code (
+// readings O2/O3/A1-A3) as a table-driven state machine, fused with the digit histograms
+// of the radix sort (B2).
+//
+// The curve is Skilling's (2004) transpose construction with x-major interleave (reading
+// A1).  Instead of running Skilling's per-bit loop (~45 ALU ops per level per cell), the
+// library derives a finite-state machine from the construction once on the host:
+//   * processing the levels top-down, everything the higher levels do to the lower bits
+//     is a signed permutation S of the three axes (the "invert X[0]" and "exchange X[0],
+//     X[i]" steps), and the final Gray-code correction is the parity p of the x^y^z bits
+//     seen above;
+//   * one level maps (S, p, octant) -> (3-bit digit, S', p').
+// The reachable (S, p) states are enumerated by BFS; two levels are composed into one
+// 64-entry row per state, so a b-bit code costs ceil(b/2) shared-memory lookups.
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "dvl_common.cuh"
+#include "dvl_internal.h"
+
+namespace dvl {
+
+namespace {
+
+// a 3-bit vector: axis 0 (x) in bit 2, axis 1 (y) in bit 1, axis 2 (z) in bit 0
+inline int bit_of(int v, int axis) { return (v >> (2 - axis)) & 1; }
+
+inline int swap_axes(int v, int a, int b) {
+  int ba = bit_of(v, a), bb = bit_of(v, b);
+  v &= ~((1 << (2 - a)) | (1 << (2 - b)));
+  return v | (bb << (2 - a)) | (ba << (2 - b));
+}
+
+struct State {
+  uint8_t map[8];   // y = S(x)
+  uint8_t parity;
+  bool operator<(const State& o) const {
+    int c = memcmp(map, o.map, 8);
+    return c != 0 ? c < 0 : parity < o.parity;
+  }
+};
+
+// One level of the construction applied to state s and input octant x.
+void step(const State& s, int x, int* digit, State* next) {
+  int y = s.map[x];
+  int y0 = bit_of(y, 0), y1 = bit_of(y, 1), y2 = bit_of(y, 2);
+  int yi[3] = {y0, y1, y2};
+  // the operations of this level on every lower level, in Skilling's order i = 0, 1, 2
+  for (int v = 0; v < 8; ++v) {
+    int w = s.map[v];
+    for (int i = 0; i < 3; ++i) w = yi[i] ? (w ^ 4) : swap_axes(w, 0, i);
+    next->map[v] = (uint8_t)w;
+  }
+  int g0 = y0, g1 = y1 ^ y0, g2 = y2 ^ y1 ^ y0;
+  int d = (g0 << 2) | (g1 << 1) | g2;
+  if (s.parity) d ^= 7;
+  *digit = d;
+  next->parity = (uint8_t)(s.parity ^ g2);
+}
+
+struct Tables {
+  int nstates = 0;
+  std::vector<uint16_t> t1;   // nstates x 8:  (next << 3) | digit
+  std::vector<uint16_t> t2;   // nstates x 64: (next << 6) | two digits
+};
+
+Tables build_tables() {
+  Tables T;
+  std::map<State, int> id;
+  std::vector<State> states;
+  State s0;
+  for (int v = 0; v < 8; ++v) s0.map[v] = (uint8_t)v;
+  s0.parity = 0;
+  id[s0] = 0;
+  states.push_back(s0);
+  std::vector<std::pair<int, int>> edges;  // (next, digit) per (state, octant)
+  for (size_t k = 0; k < states.size(); ++k) {
+    for (int x = 0; x < 8; ++x) {
+      int d;
+      State nx;
+      step(states[k], x, &d, &nx);
+      auto it = id.find(nx);
+      int j;
+      if (it == id.end()) {
+        j = (int)states.size();
+        id[nx] = j;
+        states.push_back(nx);
+      } else {
+        j = it->second;
+      }
+      edges.push_back({j, d});
+    }
+  }
+  T.nstates = (int)states.size();
+  T.t1.resize(T.nstates * 8);
+  for (int k = 0; k < T.nstates; ++k)
+    for (int x = 0; x < 8; ++x) {
+      auto e = edges[k * 8 + x];
+      T.t1[k * 8 + x] = (uint16_t)((e.first << 3) | e.second);
+    }
+  T.t2.resize(T.nstates * 64);
+  for (int k = 0; k < T.nstates; ++k)
+    for (int xh = 0; xh < 8; ++xh)
+      for (int xl = 0; xl < 8; ++xl) {
+        auto a = edges[k * 8 + xh];
+        auto b = edges[a.first * 8 + xl];
+        T.t2[k * 64 + xh * 8 + xl] = (uint16_t)((b.first << 6) | (a.second << 3) | b.second);
+      }
+  return T;
+}
+
+const Tables& tables() {
+  static Tables T = build_tables();
+  return T;
+}
+
+}  // namespace
+
+int hilbert_num_states() { return tables().nstates; }
+
+uint64_t hilbert_encode_host(uint32_t x, uint32_t y, uint32_t z, int b) {
+  const Tables& T = tables();
+  int s = 0;
+  uint64_t h = 0;
+  int j = b - 1;
+  if (b & 1) {
+    int oct = (((x >> j) & 1) << 2) | (((y >> j) & 1) << 1) | ((z >> j) & 1);
+    uint16_t e = T.t1[s * 8 + oct];
+    h = e & 7;
+    s = e >> 3;
+    --j;
+  }
+  for (; j >= 1; j -= 2) {
+    int oh = (((x >> j) & 1) << 2) | (((y >> j) & 1) << 1) | ((z >> j) & 1);
+    int ol = (((x >> (j - 1)) & 1) << 2) | (((y >> (j - 1)) & 1) << 1) | ((z >> (j - 1)) & 1);
+    uint16_t e = T.t2[s * 64 + oh * 8 + ol];
+    h = (h << 6) | (e & 63);
+    s = e >> 6;
+  }
+  return h;
+}
+
+// ----------------------------------------------------------------------- device side
+// spread the 2 bits (j, j-1) of x, y, z into the 6-bit index oh*8 + ol
+__device__ __forceinline__ int two_levels(uint32_t x, uint32_t y, uint32_t z, int j) {
+  uint32_t xb = (x >> (j - 1)) & 3, yb = (y >> (j - 1)) & 3, zb = (z >> (j - 1)) & 3;
+  // oh = (x_j, y_j, z_j), ol = (x_{j-1}, y_{j-1}, z_{j-1})
+  return (int)(((xb >> 1) << 5) | ((yb >> 1) << 4) | ((zb >> 1) << 3) | ((xb & 1) << 2) |
+               ((yb & 1) << 1) | (zb & 1));
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kBlock)
+encode_hist_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restrict__ level,
+                   int64_t n, int b, int passes, const uint16_t* __restrict__ t1g,
+                   const uint16_t* __restrict__ t2g, int nstates, K* __restrict__ keys,
+                   uint32_t* __restrict__ ids, uint32_t* __restrict__ hist) {
+  extern __shared__ uint16_t s_tab[];   // t1 (nstates*8) then t2 (nstates*64)
+  __shared__ uint32_t s_hist[8][256];
+  uint16_t* s_t1 = s_tab;
+  uint16_t* s_t2 = s_tab + nstates * 8;
+  for (int i = threadIdx.x; i < nstates * 8; i += kBlock) s_t1[i] = t1g[i];
+  for (int i = threadIdx.x; i < nstates * 64; i += kBlock) s_t2[i] = t2g[i];
+  for (int i = threadIdx.x; i < passes * 256; i += kBlock) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t h = (int64_t)blockIdx.x * kBlock + threadIdx.x; h < n;
+       h += (int64_t)gridDim.x * kBlock) {
+    uint32_t half = (1u << level[h]) >> 1;
+    uint32_t x = lower[3 * h] + half, y = lower[3 * h + 1] + half, z = lower[3 * h + 2] + half;
+    int s = 0;
+    uint64_t code = 0;
+    int j = b - 1;
+    if (b & 1) {
+      int oct = (((x >> j) & 1) << 2) | (((y >> j) & 1) << 1) | ((z >> j) & 1);
+      uint16_t e = s_t1[s * 8 + oct];
+      code = e & 7;
+      s = e >> 3;
+      --j;
+    }
+    for (; j >= 1; j -= 2) {
+      uint16_t e = s_t2[s * 64 + two_levels(x, y, z, j)];
+      code = (code << 6) | (e & 63);
+      s = e >> 6;
+    }
+    keys[h] = (K)code;
+    ids[h] = (uint32_t)h;
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(code >> (8 * p)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kBlock) {
+    uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, int b,
+                        int key_bytes, int passes, const uint16_t* d_t1, const uint16_t* d_t2,
+                        int nstates, void* keys, uint32_t* ids, uint32_t* hist, int grid,
+                        cudaStream_t st) {
+  size_t smem = (size_t)nstates * (8 + 64) * sizeof(uint16_t);
+  if (key_bytes == 4)
+    encode_hist_kernel<uint32_t><<<grid, kBlock, smem, st>>>(
+        lower, level, n, b, passes, d_t1, d_t2, nstates, (uint32_t*)keys, ids, hist);
+  else
+    encode_hist_kernel<unsigned long long><<<grid, kBlock, smem, st>>>(
+        lower, level, n, b, passes, d_t1, d_t2, nstates, (unsigned long long*)keys, ids, hist);
+}
+
+void hilbert_tables_host(std::vector<uint16_t>* t1, std::vector<uint16_t>* t2, int* nstates) {
+  const Tables& T = tables();
+  *t1 = T.t1;
+  *t2 = T.t2;
+  *nstates = T.nstates;
+}
+
+}  // namespace dvl

@@ -1,0 +1,256 @@
+"""Thin ctypes binding of the C ABI in include/dvl.h (argument marshalling only).
+
+Every step of the DVL hot path runs in the CUDA library ``libdvl.so`` built in-tree by
+``paper_2306_11612_b200/build.py``; there is no CPU fallback: if the library is missing
+this module raises.  Host arrays are numpy arrays; device arrays are torch CUDA tensors
+(PyTorch is used only for device memory and streams).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdvl.so")
+
+HOST, DEVICE = 0, 1
+MAXV_MODES = {"conservative": 0, "per_entry": 1, "exact": 2}
+STATUS = {0: "DVL_OK", 1: "DVL_E_INVAL", 2: "DVL_E_STATE", 3: "DVL_E_RANGE", 4: "DVL_E_OVERLAP",
+          5: "DVL_E_DEGENERATE", 6: "DVL_E_NOMEM", 7: "DVL_E_CUDA", 8: "DVL_E_NCCL"}
+FLAG_TIMING = 1
+
+# every symbol include/dvl.h declares (checked by tests/test_abi.py)
+SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "dvl_build",
+           "dvl_set_params", "dvl_set_domain", "dvl_update_tf", "dvl_reset_tfs",
+           "dvl_get_polylines", "dvl_info", "dvl_get_sorted", "dvl_get_sorted_data",
+           "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
+           "dvl_hilbert_encode_host", "dvl_hilbert_states"]
+
+VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
+                         ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
+
+
+class DvlError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = STATUS.get(status, str(status))
+        super().__init__(f"{self.status}: {msg}")
+
+
+class _Init(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p),
+                ("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("user", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("members", ctypes.c_uint32), ("extent", ctypes.c_uint32),
+                ("bits", ctypes.c_int32), ("Lmax", ctypes.c_int32), ("key_bytes", ctypes.c_int32),
+                ("tf_size", ctypes.c_int32), ("P", ctypes.c_float), ("eps", ctypes.c_float),
+                ("maxv_mode", ctypes.c_int32), ("shift", ctypes.c_int32), ("maxV", ctypes.c_float),
+                ("Qtot", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64),
+                ("cells_per_tile", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class _Timings(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_float) for k in ("ingest_ms", "encode_ms", "sort_ms", "gather_ms",
+                                              "maxv_ms", "weights_scan_ms", "bin_reduce_ms",
+                                              "epilogue_ms")] + \
+               [("sort_passes", ctypes.c_int32), ("launches", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libdvl.so (in-tree).  Raises if it is missing: there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run __graft_entry__.build() "
+                           "(python paper_2306_11612_b200/build.py)")
+    L = ctypes.CDLL(path)
+    P, u32, u64, i32, f32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_float
+    sig = {
+        "dvl_create": (i32, [ctypes.POINTER(_Init), ctypes.POINTER(ctypes.c_void_p)]),
+        "dvl_destroy": (None, [P]),
+        "dvl_last_error": (ctypes.c_char_p, [P]),
+        "dvl_status_string": (ctypes.c_char_p, [i32]),
+        "dvl_build": (i32, [P, u64, P, P, u32, P, i32]),
+        "dvl_set_params": (i32, [P, f32, f32, i32]),
+        "dvl_set_domain": (i32, [P, u32, f32, f32]),
+        "dvl_update_tf": (i32, [P, u32, P, u32]),
+        "dvl_reset_tfs": (i32, [P, u32]),
+        "dvl_get_polylines": (i32, [P, u32, P, i32]),
+        "dvl_info": (i32, [P, ctypes.POINTER(_Info)]),
+        "dvl_get_sorted": (i32, [P, P, P, i32]),
+        "dvl_get_sorted_data": (i32, [P, P, P, i32]),
+        "dvl_get_prefix": (i32, [P, P, i32]),
+        "dvl_get_bin_ranges": (i32, [P, u32, P, P, i32]),
+        "dvl_get_timings": (i32, [P, ctypes.POINTER(_Timings)]),
+        "dvl_stream": (P, [P]),
+        "dvl_hilbert_encode_host": (i32, [u64, P, i32, P]),
+        "dvl_hilbert_states": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array or a torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _is_device(a) -> bool:
+    return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+def hilbert_encode_host(xyz, bits: int) -> np.ndarray:
+    """The library's table-driven Hilbert encoder evaluated on the host (no GPU)."""
+    xyz = np.ascontiguousarray(np.asarray(xyz, dtype=np.uint32).reshape(-1, 3))
+    out = np.empty(len(xyz), np.uint64)
+    st = load().dvl_hilbert_encode_host(len(xyz), _ptr(xyz), bits, _ptr(out))
+    if st:
+        raise DvlError(st, "dvl_hilbert_encode_host")
+    return out
+
+
+def hilbert_states() -> int:
+    return int(load().dvl_hilbert_states())
+
+
+class Context:
+    """One dvl_ctx: a dataset on one device plus its TFs, parameters and scratch."""
+
+    def __init__(self, device: int = 0, stream=None, timing: bool = False):
+        self._lib = load()
+        init = _Init()
+        init.device = device
+        if stream is not None:
+            init.cuda_stream = stream if isinstance(stream, int) else stream.cuda_stream
+        init.flags = FLAG_TIMING if timing else 0
+        h = ctypes.c_void_p()
+        st = self._lib.dvl_create(ctypes.byref(init), ctypes.byref(h))
+        if st:
+            raise DvlError(st, "dvl_create")
+        self._h = h
+        self.M = 0
+        self.n = 0
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st: int, what: str):
+        if st:
+            msg = self._lib.dvl_last_error(self._h) or b""
+            raise DvlError(st, f"{what}: {msg.decode()}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.dvl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def stream(self) -> int:
+        return int(self._lib.dvl_stream(self._h) or 0)
+
+    # ------------------------------------------------------------------ the ABI
+    def build(self, lower, level, scalars):
+        """lower: (n,3) u32, level: (n,) u8, scalars: (M,n) f32 -- all numpy (host) or all
+        torch CUDA tensors (device)."""
+        dev = _is_device(lower)
+        if not dev:
+            lower = np.ascontiguousarray(lower, dtype=np.uint32)
+            level = np.ascontiguousarray(level, dtype=np.uint8)
+            scalars = np.ascontiguousarray(scalars, dtype=np.float32)
+            if scalars.ndim == 1:
+                scalars = scalars[None]
+        else:
+            lower, level, scalars = lower.contiguous(), level.contiguous(), scalars.contiguous()
+            if scalars.dim() == 1:
+                scalars = scalars[None]
+        n = int(level.shape[0])
+        M = int(scalars.shape[0])
+        ptrs = (ctypes.c_void_p * max(M, 1))(*[_ptr(scalars) + 4 * n * m for m in range(M)])
+        st = self._lib.dvl_build(self._h, n, _ptr(lower), _ptr(level), M, ptrs,
+                                 DEVICE if dev else HOST)
+        self._check(st, "dvl_build")
+        self.M, self.n = M, n
+
+    def set_params(self, P: float = 1.0, eps: float = 0.025, mode: str = "conservative"):
+        self._check(self._lib.dvl_set_params(self._h, P, eps, MAXV_MODES[mode]), "dvl_set_params")
+
+    def set_domain(self, member: int, lo: float, hi: float):
+        self._check(self._lib.dvl_set_domain(self._h, member, lo, hi), "dvl_set_domain")
+
+    def update_tf(self, member: int, rgba):
+        rgba = np.ascontiguousarray(rgba, dtype=np.float32).reshape(-1, 4)
+        self._check(self._lib.dvl_update_tf(self._h, member, _ptr(rgba), rgba.shape[0]),
+                    "dvl_update_tf")
+
+    def reset_tfs(self, N: int = 256):
+        self._check(self._lib.dvl_reset_tfs(self._h, N), "dvl_reset_tfs")
+
+    def get_polylines(self, W: int, out=None):
+        """Returns an (M, W) structured numpy array (VERTEX_DTYPE); with ``out`` a torch
+        CUDA tensor of >= M*W*32 bytes, writes there on the device and returns it."""
+        if out is not None and _is_device(out):
+            self._check(self._lib.dvl_get_polylines(self._h, W, _ptr(out), DEVICE),
+                        "dvl_get_polylines")
+            return out
+        res = np.empty((self.M, W), VERTEX_DTYPE) if out is None else out
+        self._check(self._lib.dvl_get_polylines(self._h, W, _ptr(res), HOST), "dvl_get_polylines")
+        return res
+
+    def info(self) -> dict:
+        i = _Info()
+        self._check(self._lib.dvl_info(self._h, ctypes.byref(i)), "dvl_info")
+        return {k: getattr(i, k) for k, _ in _Info._fields_ if k != "reserved"}
+
+    def get_sorted(self):
+        codes = np.empty(self.n, np.uint64)
+        ids = np.empty(self.n, np.uint64)
+        self._check(self._lib.dvl_get_sorted(self._h, _ptr(codes), _ptr(ids), HOST), "dvl_get_sorted")
+        return codes, ids
+
+    def get_sorted_data(self):
+        lv = np.empty(self.n, np.uint8)
+        sc = np.empty((self.M, self.n), np.float32)
+        self._check(self._lib.dvl_get_sorted_data(self._h, _ptr(lv), _ptr(sc), HOST),
+                    "dvl_get_sorted_data")
+        return lv, sc
+
+    def get_prefix(self) -> np.ndarray:
+        Q = np.empty(self.n, np.uint64)
+        self._check(self._lib.dvl_get_prefix(self._h, _ptr(Q), HOST), "dvl_get_prefix")
+        return Q
+
+    def get_bin_ranges(self, W: int):
+        lo = np.empty(W, np.uint64)
+        hi = np.empty(W, np.uint64)
+        self._check(self._lib.dvl_get_bin_ranges(self._h, W, _ptr(lo), _ptr(hi), HOST),
+                    "dvl_get_bin_ranges")
+        return lo, hi
+
+    def timings(self) -> dict:
+        t = _Timings()
+        self._check(self._lib.dvl_get_timings(self._h, ctypes.byref(t)), "dvl_get_timings")
+        return {k: getattr(t, k) for k, _ in _Timings._fields_}

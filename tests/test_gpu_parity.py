@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bit-exact on every integer / index output (codes, permutation, levels, scalars in
+curve order, maxV, shift, Q, bin ranges, counts) and on min/max; means within 1e-5
+relative (north_star); y/rgb equal the oracle's TF sample at the GPU's mean, bit for bit,
+and are within the propagated tolerance of the oracle's y."""
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+import synth
+
+pytestmark = pytest.mark.gpu
+
+f32 = np.float32
+
+
+@pytest.fixture(scope="module")
+def dvl():
+    import paper_2306_11612_b200 as m
+    m.load()
+    return m
+
+
+def make_ctx(dvl):
+    return dvl.Context(device=0)
+
+
+# ------------------------------------------------------------------------ fixtures
+def octree(E, Lmax, seed, p=0.45):
+    rng = np.random.default_rng(seed)
+    G = E >> Lmax
+    lower, level = synth.uniform_cells(G)
+    lower = (lower << np.uint32(Lmax)).astype(np.uint32)
+    level = np.full(len(level), Lmax, np.uint8)
+    for L in range(Lmax, 0, -1):
+        mask = (level == L) & (rng.random(len(level)) < p)
+        lower, level = synth.refine(lower, level, mask)
+    perm = rng.permutation(len(level))
+    return lower[perm], level[perm]
+
+
+def sparse_cells(E, n, seed, Lmax=3):
+    """n non-overlapping cells scattered in a large grid (u64 keys when 3b > 32)."""
+    rng = np.random.default_rng(seed)
+    blocks = E >> Lmax
+    ids = rng.choice(blocks ** 3, size=n, replace=False)
+    bx, by, bz = ids % blocks, (ids // blocks) % blocks, ids // blocks ** 2
+    level = rng.integers(0, Lmax + 1, size=n).astype(np.uint8)
+    w = 1 << Lmax
+    lower = np.stack([bx, by, bz], 1).astype(np.uint32) * np.uint32(w)
+    # place the level-L cell at an aligned spot inside its block
+    off = (rng.integers(0, w, size=(n, 3)) >> level[:, None].astype(np.int64)) << level[:, None].astype(np.int64)
+    lower = lower + off.astype(np.uint32)
+    return lower, level
+
+
+def scalars(n, M, seed, nan_frac=0.0):
+    rng = np.random.default_rng(seed)
+    s = (rng.standard_normal((M, n)) * rng.uniform(0.5, 3, (M, 1)) + rng.uniform(-2, 2, (M, 1))).astype(f32)
+    if nan_frac:
+        s[rng.random(s.shape) < nan_frac] = np.nan
+    return s
+
+
+def tfs_for(M, N, seed, same=False):
+    tfs = np.stack([synth.random_tf(seed + (0 if same else m), N, member=m) for m in range(M)])
+    return tfs
+
+
+def run_gpu(dvl, lower, level, scal, tfs, W, P=1.0, eps=0.025, mode="conservative", domain=None):
+    ctx = make_ctx(dvl)
+    ctx.build(lower, level, scal)
+    ctx.set_params(P, eps, mode)
+    N = tfs.shape[1]
+    if N != 256:
+        ctx.reset_tfs(N)
+    M = scal.shape[0]
+    if domain is not None:
+        d = np.asarray(domain, f32).reshape(-1, 2)
+        d = np.repeat(d, M, axis=0) if d.shape[0] == 1 else d
+        for m in range(M):
+            ctx.set_domain(m, float(d[m, 0]), float(d[m, 1]))
+    for m in range(M):
+        ctx.update_tf(m, tfs[m])
+    out = ctx.get_polylines(W)
+    res = dict(out=out, info=ctx.info(), Q=ctx.get_prefix(), ranges=ctx.get_bin_ranges(W),
+               sorted=ctx.get_sorted(), data=ctx.get_sorted_data())
+    ctx.close()
+    return res
+
+
+def check_update(U, B, tfs, g, W):
+    info = g["info"]
+    assert np.float32(info["maxV"]) == np.float32(U.maxV), (info["maxV"], U.maxV)
+    assert info["shift"] == U.s
+    assert info["Qtot"] == U.Qtot
+    assert np.array_equal(g["Q"], U.Q)
+    lo, hi = g["ranges"]
+    assert np.array_equal(lo, U.lo) and np.array_equal(hi, U.hi)
+    out, ref = g["out"], U.vertices
+    assert np.array_equal(out["count"], ref["count"])
+    assert np.array_equal(out["t_min"], ref["t_min"])
+    assert np.array_equal(out["t_max"], ref["t_max"])
+    rel = np.abs(out["t_mean"].astype(np.float64) - ref["t_mean"]) / np.maximum(np.abs(ref["t_mean"]), 1e-30)
+    bad = rel > 1e-5
+    assert not bad.any(), (rel.max(), np.argwhere(bad)[:5])
+    # y/rgb: the TF applied to the GPU mean, bit for bit (independent oracle sampler)
+    M = out.shape[0]
+    for m in range(M):
+        for x in range(0, W, max(1, W // 64)):
+            mu = float(out["t_mean"][m, x])
+            assert out["y"][m, x] == f32(o.sample(tfs[m, :, 3], mu))
+            assert out["r"][m, x] == f32(o.sample(tfs[m, :, 0], mu))
+            assert out["b"][m, x] == f32(o.sample(tfs[m, :, 2], mu))
+
+
+def check_build(B, g):
+    codes, ids = g["sorted"]
+    assert np.array_equal(codes, B.codes)
+    assert np.array_equal(ids, B.perm)
+    lv, sc = g["data"]
+    assert np.array_equal(lv, B.level_s)
+    assert np.array_equal(sc.view(np.uint32), B.scal_s.view(np.uint32))
+    info = g["info"]
+    assert info["bits"] == B.b and info["extent"] == B.E and info["Lmax"] == B.Lmax
+
+
+def parity(dvl, lower, level, scal, tfs, W, **kw):
+    B = o.build(lower, level, scal)
+    U = o.update(B, tfs, W, **kw)
+    g = run_gpu(dvl, lower, level, scal, tfs, W, **kw)
+    check_build(B, g)
+    check_update(U, B, tfs, g, W)
+    return B, U, g
+
+
+# --------------------------------------------------------------------------- tests
+def test_c1_uniform_64(dvl):
+    c = synth.make_config("C1")
+    tfs = np.stack([synth.tf_edit(1, 0, member=m) for m in range(c["M"])])
+    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"])
+
+
+@pytest.mark.parametrize("seed,E,Lmax,M,W", [(1, 32, 3, 4, 1024), (2, 64, 4, 1, 37), (3, 16, 2, 5, 3),
+                                             (4, 64, 2, 8, 4096), (5, 32, 5, 16, 1000),
+                                             (6, 16, 1, 17, 65536), (7, 32, 3, 33, 2),
+                                             (8, 16, 2, 64, 300)])
+def test_amr_octrees(dvl, seed, E, Lmax, M, W):
+    lower, level = octree(E, Lmax, seed)
+    scal = scalars(len(level), M, seed)
+    tfs = tfs_for(M, 256, 100 + seed)
+    parity(dvl, lower, level, scal, tfs, W)
+
+
+@pytest.mark.parametrize("P", [0.0, 1.0, 2.0, 3.0, 0.5, 2.5])
+@pytest.mark.parametrize("eps", [0.0, 0.025, 0.25])
+def test_params(dvl, P, eps):
+    lower, level = octree(32, 3, 11)
+    scal = scalars(len(level), 4, 12)
+    tfs = tfs_for(4, 64, 13)
+    parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps)
+
+
+@pytest.mark.parametrize("mode", ["conservative", "per_entry", "exact"])
+@pytest.mark.parametrize("same", [False, True])
+def test_maxv_modes(dvl, mode, same):
+    lower, level = octree(32, 2, 21)
+    scal = scalars(len(level), 3, 22)
+    tfs = tfs_for(3, 128, 23, same=same)
+    parity(dvl, lower, level, scal, tfs, 700, mode=mode, domain=[[-3.0, 3.0]])
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 255, 4095, 4097, 20000])
+def test_sizes_and_ragged_tails(dvl, n):
+    lower, level = sparse_cells(256, n, n)
+    scal = scalars(n, 3, n + 1)
+    tfs = tfs_for(3, 256, n + 2)
+    parity(dvl, lower, level, scal, tfs, 1024 if n > 1 else 5)
+
+
+@pytest.mark.parametrize("E,seed", [(4096, 1), (2 ** 21, 2)])
+def test_u64_keys(dvl, E, seed):
+    lower, level = sparse_cells(E, 30000, seed, Lmax=4)
+    scal = scalars(len(level), 4, seed)
+    tfs = tfs_for(4, 256, seed)
+    B, _, g = parity(dvl, lower, level, scal, tfs, 1024)
+    assert g["info"]["key_bytes"] == 8
+
+
+def test_tf_sizes(dvl):
+    lower, level = octree(16, 2, 31)
+    scal = scalars(len(level), 2, 32)
+    for N in (2, 3, 4096):
+        parity(dvl, lower, level, scal, tfs_for(2, N, 33), 256)
+
+
+def test_nan_and_inf_scalars(dvl):
+    lower, level = octree(16, 2, 41)
+    scal = scalars(len(level), 3, 42, nan_frac=0.05)
+    scal[1, :7] = np.inf
+    scal[2, 3:9] = -np.inf
+    parity(dvl, lower, level, scal, tfs_for(3, 256, 43), 128)
+
+
+def test_repeated_edits_and_determinism(dvl):
+    """C2-style repeated TF edits on one member; two runs give identical bits."""
+    lower, level = octree(32, 3, 51)
+    scal = scalars(len(level), 4, 52)
+    B = o.build(lower, level, scal)
+    ctx = make_ctx(dvl)
+    ctx.build(lower, level, scal)
+    tfs = tfs_for(4, 256, 53)
+    for m in range(4):
+        ctx.update_tf(m, tfs[m])
+    for e in range(4):
+        tfs[0] = synth.tf_edit(2, e)
+        ctx.update_tf(0, tfs[0])
+        a = ctx.get_polylines(1024)
+        b = ctx.get_polylines(1024)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+        U = o.update(B, tfs, 1024)
+        g = dict(out=a, info=ctx.info(), Q=ctx.get_prefix(), ranges=ctx.get_bin_ranges(1024))
+        check_update(U, B, tfs, g, 1024)
+    # changing W reruns only the reduction
+    for W in (2, 4096, 333):
+        a = ctx.get_polylines(W)
+        U = o.update(B, tfs, W)
+        g = dict(out=a, info=ctx.info(), Q=ctx.get_prefix(), ranges=ctx.get_bin_ranges(W))
+        check_update(U, B, tfs, g, W)
+    ctx.close()
+
+
+def test_errors(dvl):
+    ctx = make_ctx(dvl)
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.update_tf(0, synth.identity_tf())
+    assert e.value.status == "DVL_E_STATE"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.build([[0, 0, 0], [0, 0, 0]], [0, 0], [[1.0, 2.0]])
+    assert e.value.status == "DVL_E_OVERLAP"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.build([[0, 0, 0], [1, 1, 1]], [1, 0], [[1.0, 2.0]])
+    assert e.value.status == "DVL_E_OVERLAP"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.build([[1, 0, 0]], [1], [[1.0]])
+    assert e.value.status == "DVL_E_INVAL"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.build([[2 ** 21, 0, 0]], [0], [[1.0]])
+    assert e.value.status == "DVL_E_RANGE"
+    ctx.build([[0, 0, 0], [1, 0, 0]], [0, 0], [[1.0, 2.0]])
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.get_polylines(1)
+    assert e.value.status == "DVL_E_INVAL"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.update_tf(0, np.full((8, 4), 1.5, f32))
+    assert e.value.status == "DVL_E_INVAL"
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.set_params(17.0, 0.025)
+    assert e.value.status == "DVL_E_INVAL"
+    # eps = 0 and a constant TF: every weight is 0 -> degenerate
+    ctx.set_params(1.0, 0.0)
+    ctx.update_tf(0, np.zeros((256, 4), f32))
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.get_polylines(16)
+    assert e.value.status == "DVL_E_DEGENERATE"
+    ctx.set_params(1.0, 0.025)
+    ctx.get_polylines(16)
+    ctx.close()
+
+
+def test_device_buffers(dvl):
+    """Inputs and outputs as device (torch) tensors give the same result as host arrays."""
+    import torch
+    lower, level = octree(32, 3, 61)
+    scal = scalars(len(level), 4, 62)
+    tfs = tfs_for(4, 256, 63)
+    B = o.build(lower, level, scal)
+    U = o.update(B, tfs, 1024)
+    ctx = make_ctx(dvl)
+    ctx.build(torch.from_numpy(lower.astype(np.int32)).cuda(), torch.from_numpy(level).cuda(),
+              torch.from_numpy(scal).cuda())
+    for m in range(4):
+        ctx.update_tf(m, tfs[m])
+    out = torch.empty(4 * 1024 * 8, dtype=torch.int32, device="cuda")
+    ctx.get_polylines(1024, out=out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(dvl.VERTEX_DTYPE).reshape(4, 1024)
+    assert np.array_equal(got["count"], U.vertices["count"])
+    assert np.array_equal(got["t_min"], U.vertices["t_min"])
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["C2"])
+def test_full_size_config(dvl, name):
+    """BASELINE configs[1] at full size (~10.9 M cells) in the launch configuration the
+    bench times: complete comparison (the oracle finishes it in seconds)."""
+    c = synth.make_config(name)
+    tfs = np.stack([synth.tf_edit(2, 0, member=m) for m in range(c["M"])])
+    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"])
