@@ -69,6 +69,8 @@ typedef void *(*dvl_alloc_fn)(size_t bytes, void *cuda_stream, void *user);
 typedef void (*dvl_free_fn)(void *ptr, size_t bytes, void *cuda_stream, void *user);
 
 #define DVL_FLAG_TIMING 1u   /* record CUDA events around every kernel (dvl_get_timings) */
+#define DVL_FLAG_GENERIC 2u  /* use the portable one-tile-per-CTA update kernels instead of
+                                the persistent TMA-pipelined ones (always used for M > 16) */
 
 typedef struct {
     int device;             /* CUDA device ordinal */

@@ -36,6 +36,14 @@ struct Dataset {
   float2* d_tab = nullptr;              // M x N
   unsigned long long* status1 = nullptr;  // tiles
   unsigned long long* tile_prefix = nullptr;
+  // persistent TMA path (M <= 16)
+  bool tma = false;
+  TmaPlan plan{};
+  int grid = 0;                           // chunks = CTAs of both passes
+  int planN = 0;                          // TF size the plan was made for
+  int chunk_cap = 0;
+  unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
+  unsigned long long* chunk_prefix = nullptr;   // grid
 };
 
 }  // namespace
@@ -85,6 +93,7 @@ struct dvl_ctx {
   bool ev_used[PH_N] = {};
   int sort_passes = 0;
   int launches = 0;
+  int num_sms = 148;
 };
 
 namespace {
@@ -161,7 +170,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
-                d.d_rgba, d.d_tab, d.status1, d.tile_prefix};
+                d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -201,7 +210,8 @@ PowParams pow_params(float P) {
   return pw;
 }
 
-int items_for(int M) {
+int items_for(int M, bool tma) {
+  if (tma) return tma_items_for(M);
   if (M <= 4) return 16;
   if (M <= 8) return 8;
   if (M <= 16) return 4;
@@ -255,10 +265,45 @@ void stage_tf(dvl_ctx* ctx, const float* rgba, int N) {
   CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
 }
 
+// Work split of the TMA path for the current TF size: tile size from M, stage ring depth
+// from the shared-memory budget (2 CTAs/SM when two stages fit in half an SM), chunks =
+// resident CTAs.
+void ensure_plan(dvl_ctx* ctx) {
+  Dataset& d = ctx->ds;
+  if (!d.tma || d.planN == ctx->N) return;
+  TmaPlan pl{};
+  const int T = kBlock * d.items;
+  pl.tiles = d.tiles;
+  pl.stage_bytes = (uint32_t)((((size_t)d.M * T * 4 + T) + 127) & ~(size_t)127);
+  pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
+  const size_t half = 100 * 1024, full = 205 * 1024;
+  int stages = (int)((half - pl.tab_bytes) / pl.stage_bytes);
+  if (pl.tab_bytes > half || stages < 2) stages = (int)((full - pl.tab_bytes) / pl.stage_bytes);
+  pl.stages = std::min(stages, 4);
+  if (pl.stages < 2) fail(ctx, DVL_E_INVAL, "TMA plan: stage does not fit in shared memory");
+  const int bps = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl);
+  int G = std::min(d.tiles, ctx->num_sms * bps);
+  pl.tpc = (d.tiles + G - 1) / G;
+  G = (d.tiles + pl.tpc - 1) / pl.tpc;
+  if (G + 1 > d.chunk_cap) {
+    unsigned long long* cs = dalloc<unsigned long long>(ctx, G + 1);
+    unsigned long long* cp = dalloc<unsigned long long>(ctx, G);
+    dfree(ctx, d.chunk_status);
+    dfree(ctx, d.chunk_prefix);
+    d.chunk_status = cs;
+    d.chunk_prefix = cp;
+    d.chunk_cap = G + 1;
+  }
+  d.plan = pl;
+  d.grid = G;
+  d.planN = ctx->N;
+}
+
 // U0-U2: maxV, then pass 1 (weights + decoupled look-back scan).
 void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out) {
   Dataset& d = ctx->ds;
   ctx->shift = compute_shift(ctx);
+  ensure_plan(ctx);
   UpdParams p = upd_params(ctx);
   tic(ctx, PH_MAXV);
   if (ctx->mode == DVL_MAXV_EXACT) {
@@ -271,11 +316,24 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out) {
   CKLAUNCH();
   toc(ctx, PH_MAXV);
   tic(ctx, PH_WSCAN);
-  CK(cudaMemsetAsync(d.status1, 0, sizeof(unsigned long long) * d.tiles, ctx->stream));
-  CK(cudaMemsetAsync(ctx->d_ctr1, 0, sizeof(uint32_t), ctx->stream));
-  launch_weights_scan(d.items, smem_tab_ok(ctx), export_q, p, d.status1, ctx->d_ctr1,
-                      d.tile_prefix, ctx->d_qtot, q_out, d.tiles, ctx->stream);
-  CKLAUNCH();
+  if (d.tma) {
+    CK(cudaMemsetAsync(d.chunk_status, 0, sizeof(unsigned long long) * (d.grid + 1), ctx->stream));
+    launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid, d.chunk_status,
+                              reinterpret_cast<uint32_t*>(d.chunk_status + d.grid), d.chunk_prefix,
+                              ctx->d_qtot, ctx->stream);
+    CKLAUNCH();
+    if (export_q) {
+      launch_bin_reduce_tma(d.plan.tab_bytes > 0, true, p, d.plan, d.grid, d.chunk_prefix,
+                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, ctx->stream);
+      CKLAUNCH();
+    }
+  } else {
+    CK(cudaMemsetAsync(d.status1, 0, sizeof(unsigned long long) * d.tiles, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_ctr1, 0, sizeof(uint32_t), ctx->stream));
+    launch_weights_scan(d.items, smem_tab_ok(ctx), export_q, p, d.status1, ctx->d_ctr1,
+                        d.tile_prefix, ctx->d_qtot, q_out, d.tiles, ctx->stream);
+    CKLAUNCH();
+  }
   toc(ctx, PH_WSCAN);
 }
 
@@ -404,8 +462,10 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     if (!prepared) {
       CK(prepare_onesweep());
       CK(prepare_update_kernels());
+      CK(prepare_tma_kernels());
       prepared = true;
     }
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
@@ -526,7 +586,8 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.Lmax = (int)h_ing.lmax;
     d.key_bytes = 3 * d.b <= 32 ? 4 : 8;
     d.passes = (3 * d.b + 7) / 8;
-    d.items = items_for(M);
+    d.tma = M <= 16 && !(ctx->flags & DVL_FLAG_GENERIC);
+    d.items = items_for(M, d.tma);
     const int64_t T = (int64_t)kBlock * d.items;
     d.tiles = (int)((nn + T - 1) / T);
     d.n_pad = (int64_t)d.tiles * T;
@@ -793,8 +854,12 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     // restores the identity of every entry it reads, so all entries stay identity
     Acc a = ctx->acc;
     tic(ctx, PH_BREDUCE);
-    launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a, ctx->d_err,
-                      d.tiles, ctx->stream);
+    if (d.tma)
+      launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
+                            ctx->d_qtot, W, a, 0, ctx->d_err, nullptr, ctx->stream);
+    else
+      launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a, ctx->d_err,
+                        d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
     dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;

@@ -27,8 +27,10 @@ constexpr uint32_t kSortAgg = 1u << 30;
 constexpr uint32_t kSortInc = 2u << 30;
 constexpr uint32_t kSortMask = (1u << 30) - 1;
 
-constexpr float kSumScale = 281474976710656.0f;   // 2^48: fixed point of per-thread t sums
-constexpr double kSumUnscale = 1.0 / 281474976710656.0;
+// fixed point of per-thread partial t sums: round(sum * 2^40) as u64 (a thread's running
+// total over <= 2^22 cells stays < 2^63; global totals are 128-bit)
+constexpr float kSumScale = 1099511627776.0f;     // 2^40
+constexpr double kSumUnscale = 1.0 / 1099511627776.0;
 
 // error bits written by kernels
 constexpr uint32_t kErrInval = 1u;      // L > 20 or lower not a multiple of 2^L
@@ -61,6 +63,15 @@ struct UpdParams {
   uint64_t offset;         // global prefix before this device's cells (sharding)
 };
 
+// Work split of the TMA-pipelined update kernels (host-computed).
+struct TmaPlan {
+  int tiles;              // tiles of T = 256 * ITEMS cells
+  int tpc;                // tiles per chunk (one chunk per CTA)
+  int stages;             // shared-memory ring depth
+  uint32_t stage_bytes;   // M * T * 4 + T, rounded up to 128
+  uint32_t tab_bytes;     // alpha table in shared memory (0: read through L1)
+};
+
 // Per-bin accumulators of U4 (integer-exact, combined with atomics in any order).
 struct Acc {
   unsigned long long* lo;    // W: first cell (min)
@@ -90,12 +101,36 @@ __device__ __forceinline__ float norm_t(float v, float lo, float inv) {
   return x > 0.0f ? (x < 1.0f ? x : 1.0f) : 0.0f;
 }
 
+// O7 in two instructions: mul.rn.sat rounds the product, then clamps it to [0, 1] with
+// NaN -> +0 (the same value as norm_t; -0 -> +0 is checked by the parity tests).
+__device__ __forceinline__ float norm_sat(float v, float lo, float inv) {
+  float d = __fsub_rn(v, lo), t;
+  asm("mul.rn.sat.f32 %0, %1, %2;" : "=f"(t) : "f"(d), "f"(inv));
+  return t;
+}
+
+// O8 on a shared-memory slope table: `base` is the shared address of tab[0] minus
+// 8 * 0x4B000000 (mod 2^32), so the address of tab[floor(pos)] is base + 8 * bits(pos +
+// 2^23 rounded toward zero).
+__device__ __forceinline__ float sample_smem(uint32_t base, float nm1, float t) {
+  float pos = __fmul_rn(t, nm1);
+  float f = __fadd_rz(pos, 8388608.0f);
+  uint32_t addr = base + (__float_as_uint(f) << 3);
+  float a0, d;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a0), "=f"(d) : "r"(addr));
+  float fr = __fsub_rn(pos, __fsub_rn(f, 8388608.0f));
+  return __fmaf_rn(fr, d, a0);
+}
+
 // O8: piecewise-linear lookup on t * (N - 1) with the slope table tab[i] =
 // (A[i], A[i+1] - A[i]) and tab[N-1] = (A[N-1], 0): at pos = N-1 the result is A[N-1].
+// floor(pos) for 0 <= pos < 2^23 without a conversion instruction: pos + 2^23 rounded
+// toward zero is 2^23 + floor(pos) exactly; its low mantissa bits are the integer.
 __device__ __forceinline__ float sample_tab(const float2* tab, float nm1, float t) {
   float pos = __fmul_rn(t, nm1);
-  int i0 = (int)pos;
-  float fr = __fsub_rn(pos, (float)i0);
+  float f = __fadd_rz(pos, 8388608.0f);
+  int i0 = __float_as_int(f) - 0x4B000000;
+  float fr = __fsub_rn(pos, __fsub_rn(f, 8388608.0f));   // pos - (float)i0, exact
   float2 e = tab[i0];
   return __fmaf_rn(fr, e.y, e.x);
 }

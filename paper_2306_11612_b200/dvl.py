@@ -20,6 +20,7 @@ MAXV_MODES = {"conservative": 0, "per_entry": 1, "exact": 2}
 STATUS = {0: "DVL_OK", 1: "DVL_E_INVAL", 2: "DVL_E_STATE", 3: "DVL_E_RANGE", 4: "DVL_E_OVERLAP",
           5: "DVL_E_DEGENERATE", 6: "DVL_E_NOMEM", 7: "DVL_E_CUDA", 8: "DVL_E_NCCL"}
 FLAG_TIMING = 1
+FLAG_GENERIC = 2
 
 # every symbol include/dvl.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "dvl_build",
@@ -130,13 +131,13 @@ def hilbert_states() -> int:
 class Context:
     """One dvl_ctx: a dataset on one device plus its TFs, parameters and scratch."""
 
-    def __init__(self, device: int = 0, stream=None, timing: bool = False):
+    def __init__(self, device: int = 0, stream=None, timing: bool = False, generic: bool = False):
         self._lib = load()
         init = _Init()
         init.device = device
         if stream is not None:
             init.cuda_stream = stream if isinstance(stream, int) else stream.cuda_stream
-        init.flags = FLAG_TIMING if timing else 0
+        init.flags = (FLAG_TIMING if timing else 0) | (FLAG_GENERIC if generic else 0)
         h = ctypes.c_void_p()
         st = self._lib.dvl_create(ctypes.byref(init), ctypes.byref(h))
         if st:

@@ -21,8 +21,11 @@ def dvl():
     return m
 
 
-def make_ctx(dvl):
-    return dvl.Context(device=0)
+def make_ctx(dvl, generic=False):
+    return dvl.Context(device=0, generic=generic)
+
+
+PATHS = ["tma", "generic"]
 
 
 # ------------------------------------------------------------------------ fixtures
@@ -67,8 +70,9 @@ def tfs_for(M, N, seed, same=False):
     return tfs
 
 
-def run_gpu(dvl, lower, level, scal, tfs, W, P=1.0, eps=0.025, mode="conservative", domain=None):
-    ctx = make_ctx(dvl)
+def run_gpu(dvl, lower, level, scal, tfs, W, P=1.0, eps=0.025, mode="conservative", domain=None,
+            generic=False):
+    ctx = make_ctx(dvl, generic)
     ctx.build(lower, level, scal)
     ctx.set_params(P, eps, mode)
     N = tfs.shape[1]
@@ -125,40 +129,45 @@ def check_build(B, g):
     assert info["bits"] == B.b and info["extent"] == B.E and info["Lmax"] == B.Lmax
 
 
-def parity(dvl, lower, level, scal, tfs, W, **kw):
+def parity(dvl, lower, level, scal, tfs, W, generic=False, **kw):
     B = o.build(lower, level, scal)
     U = o.update(B, tfs, W, **kw)
-    g = run_gpu(dvl, lower, level, scal, tfs, W, **kw)
+    g = run_gpu(dvl, lower, level, scal, tfs, W, generic=generic, **kw)
     check_build(B, g)
     check_update(U, B, tfs, g, W)
     return B, U, g
 
 
 # --------------------------------------------------------------------------- tests
-def test_c1_uniform_64(dvl):
+@pytest.mark.parametrize("path", PATHS)
+def test_c1_uniform_64(dvl, path):
     c = synth.make_config("C1")
     tfs = np.stack([synth.tf_edit(1, 0, member=m) for m in range(c["M"])])
-    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"])
+    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"],
+           generic=path == "generic")
 
 
 @pytest.mark.parametrize("seed,E,Lmax,M,W", [(1, 32, 3, 4, 1024), (2, 64, 4, 1, 37), (3, 16, 2, 5, 3),
                                              (4, 64, 2, 8, 4096), (5, 32, 5, 16, 1000),
                                              (6, 16, 1, 17, 65536), (7, 32, 3, 33, 2),
-                                             (8, 16, 2, 64, 300)])
-def test_amr_octrees(dvl, seed, E, Lmax, M, W):
+                                             (8, 16, 2, 64, 300), (9, 64, 3, 2, 64),
+                                             (10, 64, 4, 12, 2048)])
+@pytest.mark.parametrize("path", PATHS)
+def test_amr_octrees(dvl, seed, E, Lmax, M, W, path):
     lower, level = octree(E, Lmax, seed)
     scal = scalars(len(level), M, seed)
     tfs = tfs_for(M, 256, 100 + seed)
-    parity(dvl, lower, level, scal, tfs, W)
+    parity(dvl, lower, level, scal, tfs, W, generic=path == "generic")
 
 
 @pytest.mark.parametrize("P", [0.0, 1.0, 2.0, 3.0, 0.5, 2.5])
 @pytest.mark.parametrize("eps", [0.0, 0.025, 0.25])
-def test_params(dvl, P, eps):
+@pytest.mark.parametrize("path", PATHS)
+def test_params(dvl, P, eps, path):
     lower, level = octree(32, 3, 11)
     scal = scalars(len(level), 4, 12)
     tfs = tfs_for(4, 64, 13)
-    parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps)
+    parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps, generic=path == "generic")
 
 
 @pytest.mark.parametrize("mode", ["conservative", "per_entry", "exact"])
@@ -170,12 +179,14 @@ def test_maxv_modes(dvl, mode, same):
     parity(dvl, lower, level, scal, tfs, 700, mode=mode, domain=[[-3.0, 3.0]])
 
 
-@pytest.mark.parametrize("n", [1, 2, 7, 255, 4095, 4097, 20000])
-def test_sizes_and_ragged_tails(dvl, n):
-    lower, level = sparse_cells(256, n, n)
+@pytest.mark.parametrize("n", [1, 2, 7, 255, 2047, 2049, 4095, 4097, 20000, 300001])
+@pytest.mark.parametrize("path", PATHS)
+def test_sizes_and_ragged_tails(dvl, n, path):
+    lower, level = sparse_cells(256 if n < 100000 else 1024, n, n)
     scal = scalars(n, 3, n + 1)
     tfs = tfs_for(3, 256, n + 2)
-    parity(dvl, lower, level, scal, tfs, 1024 if n > 1 else 5)
+    for W in ((5,) if n == 1 else (1024, 3, 65536)):
+        parity(dvl, lower, level, scal, tfs, W, generic=path == "generic")
 
 
 @pytest.mark.parametrize("E,seed", [(4096, 1), (2 ** 21, 2)])
@@ -291,9 +302,26 @@ def test_device_buffers(dvl):
 
 
 @pytest.mark.parametrize("name", ["C2"])
-def test_full_size_config(dvl, name):
+@pytest.mark.parametrize("path", PATHS)
+def test_full_size_config(dvl, name, path):
     """BASELINE configs[1] at full size (~10.9 M cells) in the launch configuration the
     bench times: complete comparison (the oracle finishes it in seconds)."""
     c = synth.make_config(name)
     tfs = np.stack([synth.tf_edit(2, 0, member=m) for m in range(c["M"])])
-    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"])
+    parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"],
+           generic=path == "generic")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_negative_zero_and_domain_edges(dvl, path):
+    """v = -0.0 with a domain starting at +0.0 gives (-0 - 0) * inv = -0, which the O7
+    clamp maps to +0; values at, below and above the domain bounds clamp to 0 and 1."""
+    lower, level = octree(16, 2, 71)
+    n = len(level)
+    scal = np.abs(scalars(n, 3, 72)).astype(f32)
+    scal[0, ::3] = -0.0
+    scal[1, ::5] = 0.0
+    scal[2, ::7] = 2.0
+    scal[2, 1::7] = -1.0
+    dom = np.array([[0.0, 2.0], [0.0, 1.5], [0.0, 2.0]], f32)
+    parity(dvl, lower, level, scal, tfs_for(3, 256, 73), 64, domain=dom, generic=path == "generic")
