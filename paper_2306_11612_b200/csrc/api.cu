@@ -44,6 +44,7 @@ struct Dataset {
   int chunk_cap = 0;
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
   unsigned long long* chunk_prefix = nullptr;   // grid
+  unsigned long long* tile_meta = nullptr;      // tiles x tma_meta_words(): pass-1 records
 };
 
 }  // namespace
@@ -170,7 +171,8 @@ void dfree(dvl_ctx* ctx, void* p) {
 
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
-                d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix};
+                d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
+                d.tile_meta};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -274,7 +276,8 @@ void ensure_plan(dvl_ctx* ctx) {
   TmaPlan pl{};
   const int T = kBlock * d.items;
   pl.tiles = d.tiles;
-  pl.stage_bytes = (uint32_t)((((size_t)d.M * T * 4 + T) + 127) & ~(size_t)127);
+  pl.stage_bytes =
+      (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words()) + 127) & ~(size_t)127);
   pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
   const size_t half = 100 * 1024, full = 205 * 1024;
   int stages = (int)((half - pl.tab_bytes) / pl.stage_bytes);
@@ -320,11 +323,11 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out) {
     CK(cudaMemsetAsync(d.chunk_status, 0, sizeof(unsigned long long) * (d.grid + 1), ctx->stream));
     launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid, d.chunk_status,
                               reinterpret_cast<uint32_t*>(d.chunk_status + d.grid), d.chunk_prefix,
-                              ctx->d_qtot, ctx->stream);
+                              ctx->d_qtot, d.tile_meta, ctx->stream);
     CKLAUNCH();
     if (export_q) {
       launch_bin_reduce_tma(d.plan.tab_bytes > 0, true, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, ctx->stream);
+                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, d.tile_meta, ctx->stream);
       CKLAUNCH();
     }
   } else {
@@ -676,6 +679,7 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
     d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
     d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
+    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)d.tiles * tma_meta_words());
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
   } catch (Fail& f) {
@@ -856,7 +860,7 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, 0, ctx->d_err, nullptr, ctx->stream);
+                            ctx->d_qtot, W, a, 0, ctx->d_err, nullptr, d.tile_meta, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a, ctx->d_err,
                         d.tiles, ctx->stream);

@@ -75,15 +75,16 @@ cudaError_t prepare_tma_kernels();
 int tma_items_for(int M);
 size_t tma_smem(const TmaPlan& plan);
 int tma_blocks_per_sm(int M, bool smem_tab, const TmaPlan& plan);
+int tma_meta_words();
 void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,
                                unsigned long long* chunk_status, uint32_t* ctr,
                                unsigned long long* chunk_prefix, unsigned long long* qtot,
-                               cudaStream_t st);
+                               unsigned long long* meta, cudaStream_t st);
 void launch_bin_reduce_tma(bool smem_tab, bool export_q, const UpdParams& p, const TmaPlan& plan,
                            int grid, const unsigned long long* chunk_prefix,
                            const unsigned long long* qtot, uint32_t W, const Acc& acc,
                            uint64_t cell_offset, uint32_t* err, unsigned long long* q_out,
-                           cudaStream_t st);
+                           const unsigned long long* meta, cudaStream_t st);
 size_t bin_reduce_smem(int items, int M, int N, bool smem_tab);
 
 }  // namespace dvl
