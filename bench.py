@@ -258,6 +258,7 @@ def run_native(args, rank, world, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ctx.get_polylines(W, out=out_d)
     torch.cuda.synchronize()
+    ctx.timings()
 
     def step(e, device_out=True):
         ctx.update_tf(0, edits[e])
@@ -270,6 +271,7 @@ def run_native(args, rank, world, local):
     for e in range(args.warmup):
         step(e)
     torch.cuda.synchronize()
+    ctx.timings()
 
     # ---- timed device steps
     if dist:
@@ -285,11 +287,10 @@ def run_native(args, rank, world, local):
                 flush.fill_(k & 0xff)
             evs[k][0].record(stream)
             ctx.update_tf(0, edits[args.warmup + k])
-            t_up = ctx.timings()
             ctx.get_polylines(W, out=out_d)
             evs[k][1].record(stream)
-            t_pl = ctx.timings()
-            launches += t_up["launches"] + t_pl["launches"]
+            t_pl = ctx.timings()          # synchronises; counts the step's launches
+            launches += t_pl["launches"]
             for key in kern:
                 kern[key] += t_pl[key]
     torch.cuda.synchronize()

@@ -116,7 +116,7 @@ typedef struct {
     float maxv_ms, weights_scan_ms;                      /* dvl_update_tf */
     float bin_reduce_ms, epilogue_ms;                    /* dvl_get_polylines */
     int32_t sort_passes;
-    int32_t launches;                                    /* kernels of the last call */
+    int32_t launches;     /* kernels launched since the previous dvl_get_timings call */
 } dvl_timings;
 
 /* Create a context on init->device.  out receives the handle.  Errors: INVAL (NULL

@@ -74,8 +74,8 @@ struct dvl_ctx {
   unsigned long long* d_qtot = nullptr;
   uint32_t* d_ctr1 = nullptr;
   uint32_t* d_err = nullptr;
-  float* d_stage = nullptr;          // N x 4 floats (one TF)
-  float* h_stage = nullptr;          // pinned
+  float* h_stage = nullptr;          // pinned + mapped: one TF (N x 4 floats)
+  float* d_hstage = nullptr;         // its device alias (read by the prologue kernel)
   cudaEvent_t stage_ev = nullptr;
   uint16_t* d_t1 = nullptr;
   uint16_t* d_t2 = nullptr;
@@ -241,6 +241,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.eps = ctx->eps;
   p.pw = pow_params(ctx->P);
   p.scale = pow2f(ctx->shift);
+  p.shift = ctx->shift;
   p.offset = 0;
   return p;
 }
@@ -258,13 +259,20 @@ void upload_domains(dvl_ctx* ctx) {
                      cudaMemcpyHostToDevice, ctx->stream));
 }
 
-// Copy one N x 4 TF from host memory into the device staging buffer (through pinned memory).
+// Put one N x 4 TF into the pinned, mapped staging buffer (after the previous reader of the
+// buffer has finished); the prologue kernel reads it over PCIe.
 void stage_tf(dvl_ctx* ctx, const float* rgba, int N) {
   CK(cudaEventSynchronize(ctx->stage_ev));
   memcpy(ctx->h_stage, rgba, sizeof(float) * 4 * N);
-  CK(cudaMemcpyAsync(ctx->d_stage, ctx->h_stage, sizeof(float) * 4 * N, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
+}
+
+// The fused prologue: optional TF install of `member`, pass-1 state reset, max(V_h).
+void launch_prologue(dvl_ctx* ctx, int member, int mode, unsigned long long* zero, int zero_words) {
+  Dataset& d = ctx->ds;
+  launch_tf_prologue(ctx->d_hstage, member, mode, d.M, ctx->N, d.d_rgba, d.d_tab, d.d_vmin,
+                     d.d_vmax, d.d_lo, d.d_inv, ctx->d_maxv, zero, zero_words, ctx->stream);
+  CKLAUNCH();
+  if (member >= 0) CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
 }
 
 // Work split of the TMA path for the current TF size: tile size from M, stage ring depth
@@ -302,25 +310,25 @@ void ensure_plan(dvl_ctx* ctx) {
   d.planN = ctx->N;
 }
 
-// U0-U2: maxV, then pass 1 (weights + decoupled look-back scan).
-void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out) {
+// U0-U2: (member >= 0: install the staged TF of that member), maxV, pass 1 (weights +
+// decoupled look-back scan).
+void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int member = -1) {
   Dataset& d = ctx->ds;
   ctx->shift = compute_shift(ctx);
   ensure_plan(ctx);
   UpdParams p = upd_params(ctx);
   tic(ctx, PH_MAXV);
-  if (ctx->mode == DVL_MAXV_EXACT) {
+  const bool exact = ctx->mode == DVL_MAXV_EXACT;
+  launch_prologue(ctx, member, exact ? -1 : ctx->mode, d.tma ? d.chunk_status : nullptr,
+                  d.tma ? d.grid + 1 : 0);
+  if (exact) {
     int grid = (int)(d.n_pad / ((int64_t)kBlock * d.items));
     launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);
-  } else {
-    launch_maxv_approx(ctx->mode, d.M, ctx->N, d.d_tab, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
-                       ctx->d_maxv, ctx->stream);
+    CKLAUNCH();
   }
-  CKLAUNCH();
   toc(ctx, PH_MAXV);
   tic(ctx, PH_WSCAN);
   if (d.tma) {
-    CK(cudaMemsetAsync(d.chunk_status, 0, sizeof(unsigned long long) * (d.grid + 1), ctx->stream));
     launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid, d.chunk_status,
                               reinterpret_cast<uint32_t*>(d.chunk_status + d.grid), d.chunk_prefix,
                               ctx->d_qtot, d.tile_meta, ctx->stream);
@@ -389,9 +397,7 @@ void identity_tf_host(std::vector<float>& tf, int N) {
 void set_all_tfs(dvl_ctx* ctx, const std::vector<float>& tf, int N) {
   for (int m = 0; m < ctx->ds.M; ++m) {
     stage_tf(ctx, tf.data(), N);
-    launch_tf_prepare(ctx->d_stage, N, ctx->ds.d_rgba + (size_t)m * N, ctx->ds.d_tab + (size_t)m * N,
-                      ctx->stream);
-    CKLAUNCH();
+    launch_prologue(ctx, m, -1, nullptr, 0);
   }
 }
 
@@ -473,8 +479,8 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
     ctx->d_err = dalloc<uint32_t>(ctx, 1);
-    ctx->d_stage = dalloc<float>(ctx, 4 * kMaxN);
-    CK(cudaMallocHost(&ctx->h_stage, sizeof(float) * 4 * kMaxN));
+    CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * 4 * kMaxN, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&ctx->d_hstage, ctx->h_stage, 0));
     CK(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming));
     CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
     for (int i = 0; i < PH_N; ++i) {
@@ -520,7 +526,7 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
                      uint32_t members, const float* const* scalars, dvl_mem where) {
   if (!ctx) return DVL_E_INVAL;
   ctx->err.clear();
-  ctx->launches = 0;
+
   Dataset d;
   std::vector<void*> tmp;   // temporaries freed on every exit
   auto cleanup = [&]() {
@@ -787,7 +793,7 @@ static dvl_status check_tf(dvl_ctx* ctx, const float* rgba, uint32_t N) {
 
 dvl_status dvl_update_tf(dvl_ctx* ctx, uint32_t member, const float* rgba, uint32_t N) {
   if (!ctx) return DVL_E_INVAL;
-  ctx->launches = 0;
+
   if (!ctx->built) {
     set_err(ctx, "dvl_update_tf before dvl_build");
     return DVL_E_STATE;
@@ -805,10 +811,7 @@ dvl_status dvl_update_tf(dvl_ctx* ctx, uint32_t member, const float* rgba, uint3
   try {
     CK(cudaSetDevice(ctx->device));
     stage_tf(ctx, rgba, (int)N);
-    launch_tf_prepare(ctx->d_stage, (int)N, ctx->ds.d_rgba + (size_t)member * N,
-                      ctx->ds.d_tab + (size_t)member * N, ctx->stream);
-    CKLAUNCH();
-    run_weights(ctx, false, nullptr);
+    run_weights(ctx, false, nullptr, (int)member);
   } catch (Fail& f) {
     return f.s;
   }
@@ -840,7 +843,7 @@ dvl_status dvl_reset_tfs(dvl_ctx* ctx, uint32_t N) {
 
 dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem where) {
   if (!ctx) return DVL_E_INVAL;
-  ctx->launches = 0;
+
   if (!ctx->built) {
     set_err(ctx, "dvl_get_polylines before dvl_build");
     return DVL_E_STATE;
@@ -1037,6 +1040,7 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
       if (ctx->ev_used[i]) CK(cudaEventElapsedTime(dst[i], ctx->ev[i][0], ctx->ev[i][1]));
     t->sort_passes = ctx->sort_passes;
     t->launches = ctx->launches;
+    ctx->launches = 0;
   } catch (Fail& f) {
     return f.s;
   }

@@ -60,6 +60,7 @@ struct UpdParams {
   float eps;
   PowParams pw;
   float scale;             // 2^s
+  int shift;               // s
   uint64_t offset;         // global prefix before this device's cells (sharding)
 };
 

@@ -52,6 +52,10 @@ float ordered_to_float(uint32_t u);
 // update.cu
 void launch_tf_prepare(const float* rgba_in, int N, float4* rgba_out, float2* tab_out,
                        cudaStream_t st);
+void launch_tf_prologue(const float* stage, int member, int mode, int M, int N, float4* rgba_all,
+                        float2* tab_all, const float* vmin, const float* vmax, const float* lo,
+                        const float* inv, float* maxv, unsigned long long* zero, int zero_words,
+                        cudaStream_t st);
 void launch_maxv_approx(int mode, int M, int N, const float2* tab, const float* vmin,
                         const float* vmax, const float* lo, const float* inv, float* maxv,
                         cudaStream_t st);

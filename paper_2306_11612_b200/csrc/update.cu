@@ -105,6 +105,92 @@ void launch_maxv_approx(int mode, int M, int N, const float2* tab, const float* 
   maxv_approx_kernel<<<1, 256, 0, st>>>(mode, M, N, tab, vmin, vmax, lo, inv, maxv);
 }
 
+// Fused U0 prologue of one TF edit, one block: (member >= 0) install that member's TF
+// straight from the caller-filled pinned staging buffer (mapped host memory: the 16 N
+// bytes cross PCIe inside this kernel, no separate copy), zero the pass-1 look-back state,
+// then (mode 0/1) max(V_h) as maxv_approx_kernel.
+__global__ void __launch_bounds__(1024)
+tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M, int N,
+                   float4* __restrict__ rgba_all, float2* __restrict__ tab_all,
+                   const float* __restrict__ vmin, const float* __restrict__ vmax,
+                   const float* __restrict__ lo, const float* __restrict__ inv, float* maxv,
+                   unsigned long long* zero, int zero_words) {
+  const int tid = threadIdx.x;
+  if (member >= 0) {
+    float4* rgba = rgba_all + (int64_t)member * N;
+    float2* tab = tab_all + (int64_t)member * N;
+    for (int i = tid; i < N; i += blockDim.x) {
+      float4 e = make_float4(__fadd_rn(stage[4 * i], 0.0f), __fadd_rn(stage[4 * i + 1], 0.0f),
+                             __fadd_rn(stage[4 * i + 2], 0.0f), __fadd_rn(stage[4 * i + 3], 0.0f));
+      rgba[i] = e;
+      float d = 0.0f;
+      if (i + 1 < N) d = __fsub_rn(__fadd_rn(stage[4 * i + 7], 0.0f), e.w);
+      tab[i] = make_float2(e.w, d);
+    }
+  }
+  for (int k = tid; k < zero_words; k += blockDim.x) zero[k] = 0ull;
+  if (mode < 0) return;
+  __syncthreads();   // the new table is visible to the whole block
+  __shared__ int s_i, s_j;
+  __shared__ uint32_t s_hi, s_lo;
+  if (tid == 0) {
+    s_i = N - 1;
+    s_j = 0;
+    s_hi = 0;
+    s_lo = 0xffffffffu;
+  }
+  __syncthreads();
+  const float nm1 = (float)(N - 1);
+  for (int m = tid; m < M; m += blockDim.x) {
+    float tl = norm_t(vmin[m], lo[m], inv[m]);
+    float th = norm_t(vmax[m], lo[m], inv[m]);
+    int i = (int)floorf(__fmul_rn(tl, nm1));
+    int j = (int)ceilf(__fmul_rn(th, nm1));
+    j = min(j, N - 1);
+    atomicMin(&s_i, i);
+    atomicMax(&s_j, j);
+  }
+  __syncthreads();
+  const int i = s_i, j = s_j, w = j - i + 1;
+  uint32_t hi = 0, lo_ = 0xffffffffu;
+  if (mode == 0) {
+    for (int k = tid; k < M * w; k += blockDim.x) {
+      int m = k / w, a = i + k % w;
+      uint32_t b = __float_as_uint(tab_all[m * N + a].x);   // alpha >= +0: bits order as values
+      hi = max(hi, b);
+      lo_ = min(lo_, b);
+    }
+  } else {
+    for (int a = i + tid; a <= j; a += blockDim.x) {
+      float mx = tab_all[a].x, mn = mx;
+      for (int m = 1; m < M; ++m) {
+        float v = tab_all[m * N + a].x;
+        mx = v > mx ? v : mx;
+        mn = v < mn ? v : mn;
+      }
+      hi = max(hi, __float_as_uint(__fsub_rn(mx, mn)));
+    }
+  }
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  lo_ = __reduce_min_sync(0xffffffffu, lo_);
+  if ((tid & 31) == 0) {
+    atomicMax(&s_hi, hi);
+    atomicMin(&s_lo, lo_);
+  }
+  __syncthreads();
+  if (tid == 0)
+    *maxv = mode == 0 ? __fsub_rn(__uint_as_float(s_hi), __uint_as_float(s_lo))
+                      : __uint_as_float(s_hi);
+}
+
+void launch_tf_prologue(const float* stage, int member, int mode, int M, int N, float4* rgba_all,
+                        float2* tab_all, const float* vmin, const float* vmax, const float* lo,
+                        const float* inv, float* maxv, unsigned long long* zero, int zero_words,
+                        cudaStream_t st) {
+  tf_prologue_kernel<<<1, 1024, 0, st>>>(stage, member, mode, M, N, rgba_all, tab_all, vmin, vmax,
+                                         lo, inv, maxv, zero, zero_words);
+}
+
 // ------------------------------------------------------------ per-cell weights (U1)
 // Alpha min/max over the members of ITEMS consecutive cells starting at c0, then q.
 // With STAGE, the normalised t of every (member, cell) goes to shared memory s_t laid out
