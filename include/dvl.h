@@ -182,6 +182,52 @@ dvl_status dvl_reset_tfs(dvl_ctx *ctx, uint32_t N);
  * synchronises.  Errors: STATE, INVAL, DEGENERATE (all weights are 0), CUDA. */
 dvl_status dvl_get_polylines(dvl_ctx *ctx, uint32_t W, dvl_vertex *out, dvl_mem where);
 
+/* ---- sharding: one context per GPU, each holding a contiguous range of the global curve
+ * order.  Only two things cross shards per TF edit: the scan offset (the
+ * sum of the earlier shards' fixed-point weights) and the per-pixel accumulators, which
+ * are integers and merge exactly with MIN / MAX / SUM collectives.  The caller runs the
+ * collectives (e.g. torch.distributed over NCCL); the library never links NCCL. ---------- */
+
+/* Hilbert bits of the whole dataset, used by the next dvl_build of this shard instead of
+ * the shard's own extent (codes depend on b, so all shards must agree).  0 = own extent.
+ * Errors: INVAL (bits outside [0, 21]); the build fails with RANGE if the shard's extent
+ * exceeds 2^bits. */
+dvl_status dvl_set_global_bits(dvl_ctx *ctx, int bits);
+
+typedef struct {
+    uint64_t cell_offset;   /* global curve index of this shard's first cell */
+    uint64_t n_global;      /* cells of all shards (enters the fixed-point shift s) */
+    int32_t lmax_global;    /* coarsest level of all shards (enters s) */
+    int32_t reserved;
+    const float *vmin;      /* M global finite data minima (host), or NULL: keep this shard's */
+    const float *vmax;      /* M global finite data maxima (host), or NULL */
+} dvl_shard_info;
+
+/* Declare this context a shard of a larger dataset (after dvl_build).  Resets every
+ * member's domain to the (global) data range and recomputes the weights.  Errors: STATE,
+ * INVAL (cell_offset + n > n_global, lmax below this shard's Lmax). */
+dvl_status dvl_set_shard(dvl_ctx *ctx, const dvl_shard_info *info);
+
+/* Local sum of the fixed-point weights of the last update (one u64), copied
+ * asynchronously to device memory total_dev (e.g. a slot of an all-gather buffer). */
+dvl_status dvl_shard_total(dvl_ctx *ctx, uint64_t *total_dev);
+
+/* Number of int64 words of the accumulator export for width W: 2 (W + M W) + 3 M W. */
+uint64_t dvl_shard_export_words(dvl_ctx *ctx, uint32_t W);
+
+/* Pass 2 of this shard (U3+U4) with the global scan offset and Qtot derived on the device
+ * from totals_dev[nshards] (the gathered dvl_shard_total values, shard order), then export
+ * of the per-pixel accumulators to export_dev (device, dvl_shard_export_words int64): MIN
+ * plane, MAX plane, SUM plane (see csrc/shard.cu).  Asynchronous.  Errors: STATE, INVAL. */
+dvl_status dvl_shard_reduce(dvl_ctx *ctx, uint32_t W, const uint64_t *totals_dev, int nshards,
+                            int shard, int64_t *export_dev);
+
+/* U5 from the merged export planes (element-wise MIN / MAX / SUM over all shards of the
+ * three planes): out = M x W vertices as dvl_get_polylines.  Host output synchronises.
+ * Errors: STATE, INVAL, DEGENERATE (merged Qtot = 0, checked with host output). */
+dvl_status dvl_shard_finish(dvl_ctx *ctx, uint32_t W, const int64_t *merged_dev,
+                            dvl_vertex *out, dvl_mem where);
+
 /* ---- introspection / validation exports (copy-out; not on the timed path) ---------- */
 
 /* Scalars describing the dataset and the last update.  Synchronises. */

@@ -449,11 +449,21 @@ uint64_t or_prefix(int64_t n, const uint64_t *q, uint64_t *Q)
 
 /* O13 (A14): projection of (xf1, xf2) = (E W/Qtot, Q W/Qtot) onto bins:
  * b1 = min(W-1, floor(E W / Qtot)); b2 = min(W-1, max(b1, ceil(Q W / Qtot) - 1)). */
+void or_bins_ext(int64_t n, const uint64_t *Q, uint64_t E0, uint64_t Qtot, uint32_t W,
+                 int32_t *b1, int32_t *b2);
+
 void or_bins(int64_t n, const uint64_t *Q, uint32_t W, int32_t *b1, int32_t *b2)
 {
-    uint64_t Qtot = Q[n - 1];
+    or_bins_ext(n, Q, 0, Q[n - 1], W, b1, b2);
+}
+
+/* the same for a contiguous piece of the cells: E of its first cell is E0, the total of
+ * all cells Qtot (a shard of the curve order). */
+void or_bins_ext(int64_t n, const uint64_t *Q, uint64_t E0, uint64_t Qtot, uint32_t W,
+                 int32_t *b1, int32_t *b2)
+{
     for (int64_t h = 0; h < n; h++) {
-        unsigned __int128 E = h ? Q[h - 1] : 0;
+        unsigned __int128 E = h ? Q[h - 1] : E0;
         unsigned __int128 q = Q[h];
         unsigned __int128 x1 = (E * W) / Qtot;
         int64_t a = (int64_t)(x1 > (unsigned __int128)(W - 1) ? (W - 1) : x1);

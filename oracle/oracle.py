@@ -68,6 +68,7 @@ def lib():
             "or_weights": (None, [i64, i32, i32, P, P, P, P, P, f32, f32, f32, i32, P, P]),
             "or_prefix": (u64, [i64, P, P]),
             "or_bins": (None, [i64, P, ctypes.c_uint32, P, P]),
+            "or_bins_ext": (None, [i64, P, u64, u64, ctypes.c_uint32, P, P]),
             "or_reduce": (None, [i64, i32, i32, P, P, P, P, ctypes.c_uint32, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -184,6 +185,15 @@ def shift(n_global: int, Lmax: int, P: float) -> int:
 
 def fixed(f: float, s: int) -> int:
     return int(lib().or_fixed(f, s))
+
+
+def bins_ext(Q, E0: int, Qtot: int, W: int):
+    """O13 on a contiguous piece of the cells (first cell's E = E0, total Qtot)."""
+    Q = np.ascontiguousarray(Q, dtype=np.uint64)
+    b1 = np.empty(len(Q), np.int32)
+    b2 = np.empty(len(Q), np.int32)
+    lib().or_bins_ext(len(Q), _p(Q), E0, Qtot, W, _p(b1), _p(b2))
+    return b1, b2
 
 
 def identity_tf(N: int = 256) -> np.ndarray:

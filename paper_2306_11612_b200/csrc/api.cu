@@ -95,6 +95,14 @@ struct dvl_ctx {
   int sort_passes = 0;
   int launches = 0;
   int num_sms = 148;
+
+  // sharding (dvl_set_global_bits / dvl_set_shard)
+  int global_bits = 0;
+  bool sharded = false;
+  uint64_t cell_offset = 0, n_global = 0;
+  int lmax_global = 0;
+  unsigned long long* d_offset = nullptr;      // global scan offset of this shard
+  unsigned long long* d_qtot_glob = nullptr;   // global Qtot
 };
 
 namespace {
@@ -246,9 +254,14 @@ UpdParams upd_params(dvl_ctx* ctx) {
   return p;
 }
 
-// O11: s = 61 - ceil(log2 n) - ceil(Lmax P)
+int lmax_eff(const dvl_ctx* ctx) {
+  return ctx->sharded ? std::max(ctx->lmax_global, ctx->ds.Lmax) : ctx->ds.Lmax;
+}
+
+// O11: s = 61 - ceil(log2 n) - ceil(Lmax P), over the whole (possibly sharded) dataset
 int compute_shift(dvl_ctx* ctx) {
-  return 61 - ceil_log2_u64((uint64_t)ctx->ds.n) - ceil_lmax_p(ctx->ds.Lmax, ctx->P);
+  const uint64_t n = ctx->sharded ? ctx->n_global : (uint64_t)ctx->ds.n;
+  return 61 - ceil_log2_u64(n) - ceil_lmax_p(lmax_eff(ctx), ctx->P);
 }
 
 void upload_domains(dvl_ctx* ctx) {
@@ -479,6 +492,8 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
     ctx->d_err = dalloc<uint32_t>(ctx, 1);
+    ctx->d_offset = dalloc<unsigned long long>(ctx, 1);
+    ctx->d_qtot_glob = dalloc<unsigned long long>(ctx, 1);
     CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * 4 * kMaxN, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ctx->d_hstage, ctx->h_stage, 0));
     CK(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming));
@@ -592,6 +607,10 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.M = M;
     d.E = (uint32_t)h_ing.extent;
     d.b = std::max(1, ceil_log2_u64(h_ing.extent));
+    if (ctx->global_bits > 0) {
+      if (d.b > ctx->global_bits) fail(ctx, DVL_E_RANGE, "shard extent exceeds 2^global_bits");
+      d.b = ctx->global_bits;
+    }
     d.Lmax = (int)h_ing.lmax;
     d.key_bytes = 3 * d.b <= 32 ? 4 : 8;
     d.passes = (3 * d.b + 7) / 8;
@@ -698,6 +717,10 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
   free_dataset(ctx, ctx->ds);
   ctx->ds = d;
   ctx->built = true;
+  ctx->sharded = false;
+  ctx->cell_offset = 0;
+  ctx->n_global = (uint64_t)d.n;
+  ctx->lmax_global = d.Lmax;
   ctx->N = 256;
   ctx->lo_h = ctx->ds.vmin;
   ctx->hi_h = ctx->ds.vmax;
@@ -736,7 +759,7 @@ dvl_status dvl_set_params(dvl_ctx* ctx, float P, float eps, dvl_maxv_mode mode) 
     set_err(ctx, "bad maxV mode");
     return DVL_E_INVAL;
   }
-  if (ctx->built && ceil_lmax_p(ctx->ds.Lmax, P) > 100) {
+  if (ctx->built && ceil_lmax_p(lmax_eff(ctx), P) > 100) {
     set_err(ctx, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
     return DVL_E_RANGE;
   }
@@ -863,10 +886,11 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, 0, ctx->d_err, nullptr, d.tile_meta, ctx->stream);
+                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta,
+                            ctx->stream);
     else
-      launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a, ctx->d_err,
-                        d.tiles, ctx->stream);
+      launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
+                        ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
     dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
@@ -880,6 +904,161 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
                          cudaMemcpyDeviceToHost, ctx->stream));
     }
     if (where == DVL_MEM_HOST || maybe_degenerate(ctx)) {
+      uint32_t herr = 0;
+      CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (herr & kErrDegenerate) {
+        CK(cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
+        ctx->last_W = 0;
+        fail(ctx, DVL_E_DEGENERATE, "all weights are 0 (Qtot = 0)");
+      }
+    }
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_set_global_bits(dvl_ctx* ctx, int bits) {
+  if (!ctx) return DVL_E_INVAL;
+  if (bits < 0 || bits > 21) {
+    set_err(ctx, "global bits must be in [0, 21]");
+    return DVL_E_INVAL;
+  }
+  ctx->global_bits = bits;
+  return DVL_OK;
+}
+
+dvl_status dvl_set_shard(dvl_ctx* ctx, const dvl_shard_info* info) {
+  if (!ctx || !info) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_set_shard before dvl_build");
+    return DVL_E_STATE;
+  }
+  const Dataset& d = ctx->ds;
+  if (info->cell_offset + (uint64_t)d.n > info->n_global || info->n_global >= (1ull << 40) ||
+      info->lmax_global < d.Lmax || info->lmax_global > 20) {
+    set_err(ctx, "inconsistent shard description");
+    return DVL_E_INVAL;
+  }
+  if (ceil_lmax_p(info->lmax_global, ctx->P) > 100) {
+    set_err(ctx, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
+    return DVL_E_RANGE;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->sharded = true;
+    ctx->cell_offset = info->cell_offset;
+    ctx->n_global = info->n_global;
+    ctx->lmax_global = info->lmax_global;
+    Dataset& dd = ctx->ds;
+    if (info->vmin && info->vmax) {
+      for (int m = 0; m < dd.M; ++m) {
+        dd.vmin[m] = info->vmin[m];
+        dd.vmax[m] = info->vmax[m];
+      }
+      CK(cudaMemcpyAsync(dd.d_vmin, dd.vmin.data(), 4 * dd.M, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(dd.d_vmax, dd.vmax.data(), 4 * dd.M, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->lo_h = dd.vmin;
+    ctx->hi_h = dd.vmax;
+    for (int m = 0; m < dd.M; ++m)
+      ctx->inv_h[m] = ctx->hi_h[m] > ctx->lo_h[m] ? 1.0f / (ctx->hi_h[m] - ctx->lo_h[m]) : 0.0f;
+    upload_domains(ctx);
+    run_weights(ctx, false, nullptr);
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_shard_total(dvl_ctx* ctx, uint64_t* total_dev) {
+  if (!ctx || !total_dev) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "no dataset");
+    return DVL_E_STATE;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(total_dev, ctx->d_qtot, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+uint64_t dvl_shard_export_words(dvl_ctx* ctx, uint32_t W) {
+  if (!ctx || !ctx->built) return 0;
+  const uint64_t MW = (uint64_t)ctx->ds.M * W;
+  return 2 * (W + MW) + 3 * MW;
+}
+
+dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev, int nshards,
+                            int shard, int64_t* export_dev) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_shard_reduce before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (W < 2 || W > kMaxW || !totals_dev || !export_dev || nshards < 1 || shard < 0 ||
+      shard >= nshards) {
+    set_err(ctx, "bad shard reduce arguments");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    ensure_acc(ctx, W);
+    Dataset& d = ctx->ds;
+    launch_shard_offsets((const unsigned long long*)totals_dev, nshards, shard, ctx->d_offset,
+                         ctx->d_qtot_glob, ctx->stream);
+    CKLAUNCH();
+    UpdParams p = upd_params(ctx);
+    p.offset_dev = ctx->d_offset;
+    Acc a = ctx->acc;
+    tic(ctx, PH_BREDUCE);
+    if (d.tma)
+      launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
+                            ctx->d_qtot_glob, W, a, ctx->cell_offset, ctx->d_err, nullptr,
+                            d.tile_meta, ctx->stream);
+    else
+      launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
+                        ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
+    CKLAUNCH();
+    toc(ctx, PH_BREDUCE);
+    launch_acc_export(a, W, d.M, (long long*)export_dev, ctx->stream);
+    CKLAUNCH();
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_shard_finish(dvl_ctx* ctx, uint32_t W, const int64_t* merged_dev, dvl_vertex* out,
+                            dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_shard_finish before dvl_build");
+    return DVL_E_STATE;
+  }
+  if (W < 2 || W > kMaxW || !merged_dev || !out || (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE)) {
+    set_err(ctx, "bad shard finish arguments");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    ensure_acc(ctx, W);
+    Dataset& d = ctx->ds;
+    dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
+    tic(ctx, PH_EPI);
+    launch_epilogue_merged((const long long*)merged_dev, W, d.M, ctx->N, d.d_rgba, dst,
+                           ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
+    CKLAUNCH();
+    toc(ctx, PH_EPI);
+    ctx->last_W = W;
+    if (where == DVL_MEM_HOST) {
+      CK(cudaMemcpyAsync(out, ctx->d_out, sizeof(dvl_vertex) * (size_t)W * d.M,
+                         cudaMemcpyDeviceToHost, ctx->stream));
       uint32_t herr = 0;
       CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));

@@ -61,7 +61,8 @@ struct UpdParams {
   PowParams pw;
   float scale;             // 2^s
   int shift;               // s
-  uint64_t offset;         // global prefix before this device's cells (sharding)
+  uint64_t offset;         // global prefix before this device's cells (sharding, host part)
+  const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
 };
 
 // Work split of the TMA-pipelined update kernels (host-computed).

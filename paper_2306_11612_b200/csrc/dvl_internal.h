@@ -66,7 +66,16 @@ void launch_weights_scan(int items, bool smem_tab, bool export_q, const UpdParam
                          unsigned long long* q_out, int tiles, cudaStream_t st);
 void launch_bin_reduce(int items, bool smem_tab, const UpdParams& p,
                        const unsigned long long* tile_prefix, const unsigned long long* qtot,
-                       uint32_t W, const Acc& acc, uint32_t* err, int tiles, cudaStream_t st);
+                       uint32_t W, const Acc& acc, uint64_t cell_offset, uint32_t* err, int tiles,
+                       cudaStream_t st);
+
+// shard.cu
+void launch_shard_offsets(const unsigned long long* totals, int nshards, int shard,
+                          unsigned long long* offset, unsigned long long* qtot, cudaStream_t st);
+void launch_acc_export(const Acc& acc, uint32_t W, int M, long long* out, cudaStream_t st);
+void launch_epilogue_merged(const long long* merged, uint32_t W, int M, int N, const float4* rgba,
+                            dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
+                            cudaStream_t st);
 void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                      cudaStream_t st);

@@ -394,7 +394,8 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
   __syncthreads();
   unsigned long long wpre = 0;
   for (int w = 0; w < warp; ++w) wpre += s_warp[w];
-  const unsigned long long base = p.offset + tile_prefix[tile] + wpre + wincl - tsum;
+  const unsigned long long base =
+      p.offset + (p.offset_dev ? *p.offset_dev : 0ull) + tile_prefix[tile] + wpre + wincl - tsum;
 
   // bins: b1 = min(W-1, max{x : ceil(x Qtot/W) <= E}), b2 = min(W-1, max(b1, max{x <= W-1 :
   // floor(x Qtot/W) < Q})).  T(x) = x a + ceil(x r / W), T'(x) = x a + floor(x r / W).
@@ -720,23 +721,24 @@ void launch_weights_scan(int items, bool smem_tab, bool export_q, const UpdParam
 template <int ITEMS>
 static void br_dispatch(bool smem_tab, const UpdParams& p, const unsigned long long* tp,
                         const unsigned long long* qtot, uint32_t W, const Acc& acc,
-                        uint32_t* err, int tiles, cudaStream_t st) {
+                        uint64_t cell_offset, uint32_t* err, int tiles, cudaStream_t st) {
   size_t sm = bin_reduce_smem(ITEMS, p.M, p.N, smem_tab);
   if (smem_tab)
-    bin_reduce_kernel<ITEMS, true><<<tiles, kBlock, sm, st>>>(p, tp, qtot, W, acc, 0, err);
+    bin_reduce_kernel<ITEMS, true><<<tiles, kBlock, sm, st>>>(p, tp, qtot, W, acc, cell_offset, err);
   else
-    bin_reduce_kernel<ITEMS, false><<<tiles, kBlock, sm, st>>>(p, tp, qtot, W, acc, 0, err);
+    bin_reduce_kernel<ITEMS, false><<<tiles, kBlock, sm, st>>>(p, tp, qtot, W, acc, cell_offset, err);
 }
 
 void launch_bin_reduce(int items, bool smem_tab, const UpdParams& p,
                        const unsigned long long* tile_prefix, const unsigned long long* qtot,
-                       uint32_t W, const Acc& acc, uint32_t* err, int tiles, cudaStream_t st) {
+                       uint32_t W, const Acc& acc, uint64_t cell_offset, uint32_t* err, int tiles,
+                       cudaStream_t st) {
   switch (items) {
-    case 16: br_dispatch<16>(smem_tab, p, tile_prefix, qtot, W, acc, err, tiles, st); break;
-    case 8: br_dispatch<8>(smem_tab, p, tile_prefix, qtot, W, acc, err, tiles, st); break;
-    case 4: br_dispatch<4>(smem_tab, p, tile_prefix, qtot, W, acc, err, tiles, st); break;
-    case 2: br_dispatch<2>(smem_tab, p, tile_prefix, qtot, W, acc, err, tiles, st); break;
-    default: br_dispatch<1>(smem_tab, p, tile_prefix, qtot, W, acc, err, tiles, st); break;
+    case 16: br_dispatch<16>(smem_tab, p, tile_prefix, qtot, W, acc, cell_offset, err, tiles, st); break;
+    case 8: br_dispatch<8>(smem_tab, p, tile_prefix, qtot, W, acc, cell_offset, err, tiles, st); break;
+    case 4: br_dispatch<4>(smem_tab, p, tile_prefix, qtot, W, acc, cell_offset, err, tiles, st); break;
+    case 2: br_dispatch<2>(smem_tab, p, tile_prefix, qtot, W, acc, cell_offset, err, tiles, st); break;
+    default: br_dispatch<1>(smem_tab, p, tile_prefix, qtot, W, acc, cell_offset, err, tiles, st); break;
   }
 }
 

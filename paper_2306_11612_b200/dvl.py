@@ -27,7 +27,9 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_set_params", "dvl_set_domain", "dvl_update_tf", "dvl_reset_tfs",
            "dvl_get_polylines", "dvl_info", "dvl_get_sorted", "dvl_get_sorted_data",
            "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
-           "dvl_hilbert_encode_host", "dvl_hilbert_states"]
+           "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
+           "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
+           "dvl_shard_finish"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -52,6 +54,12 @@ class _Info(ctypes.Structure):
                 ("maxv_mode", ctypes.c_int32), ("shift", ctypes.c_int32), ("maxV", ctypes.c_float),
                 ("Qtot", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64),
                 ("cells_per_tile", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class _ShardInfo(ctypes.Structure):
+    _fields_ = [("cell_offset", ctypes.c_uint64), ("n_global", ctypes.c_uint64),
+                ("lmax_global", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("vmin", ctypes.c_void_p), ("vmax", ctypes.c_void_p)]
 
 
 class _Timings(ctypes.Structure):
@@ -94,6 +102,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_stream": (P, [P]),
         "dvl_hilbert_encode_host": (i32, [u64, P, i32, P]),
         "dvl_hilbert_states": (i32, []),
+        "dvl_set_global_bits": (i32, [P, i32]),
+        "dvl_set_shard": (i32, [P, ctypes.POINTER(_ShardInfo)]),
+        "dvl_shard_total": (i32, [P, P]),
+        "dvl_shard_export_words": (u64, [P, u32]),
+        "dvl_shard_reduce": (i32, [P, u32, P, i32, i32, P]),
+        "dvl_shard_finish": (i32, [P, u32, P, P, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -250,6 +264,44 @@ class Context:
         self._check(self._lib.dvl_get_bin_ranges(self._h, W, _ptr(lo), _ptr(hi), HOST),
                     "dvl_get_bin_ranges")
         return lo, hi
+
+    # ------------------------------------------------------------------ sharding
+    def set_global_bits(self, bits: int):
+        self._check(self._lib.dvl_set_global_bits(self._h, bits), "dvl_set_global_bits")
+
+    def set_shard(self, cell_offset: int, n_global: int, lmax_global: int, vmin=None, vmax=None):
+        info = _ShardInfo()
+        info.cell_offset, info.n_global, info.lmax_global = cell_offset, n_global, lmax_global
+        keep = []
+        if vmin is not None:
+            vmin = np.ascontiguousarray(vmin, np.float32)
+            vmax = np.ascontiguousarray(vmax, np.float32)
+            keep = [vmin, vmax]
+            info.vmin, info.vmax = _ptr(vmin), _ptr(vmax)
+        self._check(self._lib.dvl_set_shard(self._h, ctypes.byref(info)), "dvl_set_shard")
+        del keep
+
+    def shard_total(self, dst):
+        """Copy this shard's weight total into dst (a torch CUDA int64 tensor element)."""
+        self._check(self._lib.dvl_shard_total(self._h, _ptr(dst)), "dvl_shard_total")
+
+    def shard_export_words(self, W: int) -> int:
+        return int(self._lib.dvl_shard_export_words(self._h, W))
+
+    def shard_reduce(self, W: int, totals, shard: int, export):
+        """totals: CUDA int64 tensor [nshards]; export: CUDA int64 tensor of export words."""
+        self._check(self._lib.dvl_shard_reduce(self._h, W, _ptr(totals), int(totals.numel()),
+                                               shard, _ptr(export)), "dvl_shard_reduce")
+
+    def shard_finish(self, W: int, merged, out=None):
+        if out is not None and _is_device(out):
+            self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(out), DEVICE),
+                        "dvl_shard_finish")
+            return out
+        res = np.empty((self.M, W), VERTEX_DTYPE)
+        self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(res), HOST),
+                    "dvl_shard_finish")
+        return res
 
     def timings(self) -> dict:
         t = _Timings()
