@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--build-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded path (collectives) even at N=1")
     return ap.parse_args()
 
 
@@ -221,17 +223,35 @@ def run_native(args, rank, world, local):
     args_cfg_name = args.config
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"),
+                     ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    c = workload(args.config)
+    import synth
+    # sharded (N > 1): weak scaling over a 2x larger logical grid whose first `world`
+    # octants in curve order each hold one rank's config-sized piece -- every rank owns one
+    # contiguous range of the global Hilbert order (codes with one more bit)
+    c = synth.make_config(args.config, seed=synth.CELL_SEED + (rank if sharded else 0))
     n = len(c["level"])
     M, W, N = c["M"], c["W"], 256
     base, edits = tf_sequence(args.config, args.warmup + args.steps, N, M)
+    gbits = 0
+    if sharded:
+        b0 = int(np.ceil(np.log2(c["E"])))
+        gbits = b0 + 1
+        half = np.uint32(1 << b0)
+        corners = np.array([[x, y, z] for x in (0, 1) for y in (0, 1) for z in (0, 1)], np.uint32) * half
+        order = np.argsort(dvl.hilbert_encode_host(corners, gbits))
+        c["lower"] = (c["lower"] + corners[order[rank]]).astype(np.uint32)
 
     stream = torch.cuda.Stream()
     ctx = dvl.Context(device=local, stream=stream, timing=True)
+    if gbits:
+        ctx.set_global_bits(gbits)
     dev = torch.device("cuda", local)
     lower_d = torch.from_numpy(c["lower"].view(np.int32)).to(dev)
     level_d = torch.from_numpy(c["level"]).to(dev)
@@ -250,22 +270,36 @@ def run_native(args, rank, world, local):
             build_ms.append(ev0.elapsed_time(ev1))
             phase.append(ctx.timings())
     info = ctx.info()
+    domain = c["domain"]
+    polylines = ctx.get_polylines
+    if sharded:
+        from paper_2306_11612_b200.shard import ShardedContext
+        sc = ShardedContext(ctx)
+        fin = np.where(np.isfinite(c["scal"]), c["scal"], np.nan)
+        sc.describe(n, int(info["Lmax"]), np.nanmin(fin, axis=1), np.nanmax(fin, axis=1))
+        if domain is not None:   # shared domain: union over all ranks
+            d = torch.tensor(domain, device=dev)
+            lo_, hi_ = d[:, 0].contiguous(), d[:, 1].contiguous()
+            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
+            dist.all_reduce(hi_, op=dist.ReduceOp.MAX)
+            domain = torch.stack([lo_, hi_], 1).cpu().numpy()
+        polylines = sc.get_polylines
     for m in range(M):
-        if c["domain"] is not None:
-            ctx.set_domain(m, float(c["domain"][m, 0]), float(c["domain"][m, 1]))
+        if domain is not None:
+            ctx.set_domain(m, float(domain[m, 0]), float(domain[m, 1]))
         ctx.update_tf(m, base[m])
     out_d = torch.empty(M * W * 8, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    ctx.get_polylines(W, out=out_d)
+    polylines(W, out=out_d)
     torch.cuda.synchronize()
     ctx.timings()
 
     def step(e, device_out=True):
         ctx.update_tf(0, edits[e])
         if device_out:
-            ctx.get_polylines(W, out=out_d)
+            polylines(W, out=out_d)
         else:
-            return ctx.get_polylines(W)
+            return polylines(W)
 
     # ---- warm-up
     for e in range(args.warmup):
@@ -287,7 +321,7 @@ def run_native(args, rank, world, local):
                 flush.fill_(k & 0xff)
             evs[k][0].record(stream)
             ctx.update_tf(0, edits[args.warmup + k])
-            ctx.get_polylines(W, out=out_d)
+            polylines(W, out=out_d)
             evs[k][1].record(stream)
             t_pl = ctx.timings()          # synchronises; counts the step's launches
             launches += t_pl["launches"]
@@ -313,7 +347,7 @@ def run_native(args, rank, world, local):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx.update_tf(0, edits[args.warmup + k])
-        res = ctx.get_polylines(W)   # host output: synchronises
+        res = polylines(W)   # host output: synchronises
         e2e_times.append(time.perf_counter() - t0)
     e2e_ms = 1e3 * sum(e2e_times) / len(e2e_times)
     if dist:
@@ -321,6 +355,8 @@ def run_native(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     assert res["count"].sum() >= n
+    if sharded:
+        dist.barrier()
 
     if rank != 0:
         dist.destroy_process_group()
@@ -333,7 +369,9 @@ def run_native(args, rank, world, local):
     dom = max(bytes_cell, key=lambda k: per_kernel[k])
     alg_bytes = n * bytes_cell[dom]
     achieved = alg_bytes / (per_kernel[dom] / 1e3) / 1e9
-    kname = {"weights_scan_ms": "weights_scan_kernel", "bin_reduce_ms": "bin_reduce_kernel"}[dom]
+    tma = M <= 16
+    kname = {"weights_scan_ms": "weights_reduce_tma" if tma else "weights_scan_kernel",
+             "bin_reduce_ms": "bin_reduce_tma" if tma else "bin_reduce_kernel"}[dom]
     traffic = load_traffic(kname)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -358,7 +396,8 @@ def run_native(args, rank, world, local):
                    "n_cells": n, "members": M, "W": W, "tf_size": N, "levels": int(info["Lmax"]) + 1,
                    "bits": info["bits"], "edits": "member 0, new random TF per step",
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": "replicas" if world > 1 else "single"},
+                   "parallelism": f"sharded-dp{world}" if sharded else "single",
+                   "cells_per_gpu": n, "global_bits": gbits or info["bits"]},
         "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90))},
         "kernels_ms": per_kernel,
