@@ -147,7 +147,7 @@ void* dmalloc(dvl_ctx* ctx, size_t bytes) {
     p = ctx->alloc(bytes, (void*)ctx->stream, ctx->user);
     if (!p) fail(ctx, DVL_E_NOMEM, "device allocation of " + std::to_string(bytes) + " B failed");
   } else {
-    cudaError_t e = cudaMalloc(&p, bytes);
+    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);   // stream-ordered pool
     if (e != cudaSuccess) {
       cudaGetLastError();
       fail(ctx, DVL_E_NOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
@@ -174,7 +174,7 @@ void dfree(dvl_ctx* ctx, void* p) {
   if (ctx->free)
     ctx->free(p, bytes, (void*)ctx->stream, ctx->user);
   else
-    cudaFree(p);
+    cudaFreeAsync(p, ctx->stream);
 }
 
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
@@ -474,6 +474,14 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     ctx->user = init->user;
     ctx->flags = init->flags;
     CK(cudaSetDevice(ctx->device));
+    {
+      // keep freed blocks in the device's default pool (rebuilds reuse them)
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    }
     if (init->cuda_stream) {
       ctx->stream = (cudaStream_t)init->cuda_stream;
     } else {
@@ -528,6 +536,7 @@ void dvl_destroy(dvl_ctx* ctx) {
   std::vector<void*> ps;
   for (auto& kv : ctx->live) ps.push_back(kv.first);
   for (void* p : ps) dfree(ctx, p);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->stage_ev) cudaEventDestroy(ctx->stage_ev);
   for (int i = 0; i < PH_N; ++i)
@@ -665,12 +674,17 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     for (int p = 0; p < d.passes; ++p) {
       uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
       if ((int64_t)mx == nn) continue;
-      launch_onesweep(kin, vin, kout, vout, nn, kb, 8 * p, base + p * 256,
+      // the first pass generates the ids (iota) instead of reading them
+      launch_onesweep(kin, done == 0 ? nullptr : vin, kout, vout, nn, kb, 8 * p, base + p * 256,
                       status + (size_t)p * stiles * 256, ctrs + p, st);
       CKLAUNCH();
       std::swap(kin, kout);
       std::swap(vin, vout);
       ++done;
+    }
+    if (done == 0) {   // every digit constant (n == 1): the identity permutation
+      launch_iota(vin, nn, st);
+      CKLAUNCH();
     }
     ctx->sort_passes = done;
     toc(ctx, PH_SORT);

@@ -18,6 +18,7 @@ struct Acc;
 int hilbert_num_states();
 uint64_t hilbert_encode_host(uint32_t x, uint32_t y, uint32_t z, int b);
 void hilbert_tables_host(std::vector<uint16_t>* t1, std::vector<uint16_t>* t2, int* nstates);
+void launch_iota(uint32_t* v, int64_t n, cudaStream_t st);
 void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, int b,
                         int key_bytes, int passes, const uint16_t* d_t1, const uint16_t* d_t2,
                         int nstates, void* keys, uint32_t* ids, uint32_t* hist, int grid,

@@ -12,6 +12,7 @@
 //   * one level maps (S, p, octant) -> (3-bit digit, S', p').
 // The reachable (S, p) states are enumerated by BFS; two levels are composed into one
 // 64-entry row per state, so a b-bit code costs ceil(b/2) shared-memory lookups.
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -183,8 +184,7 @@ encode_hist_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restrict
       code = (code << 6) | (e & 63);
       s = e >> 6;
     }
-    keys[h] = (K)code;
-    ids[h] = (uint32_t)h;
+    keys[h] = (K)code;   // the ids (0..n-1) are implicit in the first sort pass
     for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(code >> (8 * p)) & 255], 1u);
   }
   __syncthreads();
@@ -205,6 +205,16 @@ void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, 
   else
     encode_hist_kernel<unsigned long long><<<grid, kBlock, smem, st>>>(
         lower, level, n, b, passes, d_t1, d_t2, nstates, (unsigned long long*)keys, ids, hist);
+}
+
+__global__ void iota_kernel(uint32_t* v, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    v[k] = (uint32_t)k;
+}
+
+void launch_iota(uint32_t* v, int64_t n, cudaStream_t st) {
+  iota_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(v, n);
 }
 
 void hilbert_tables_host(std::vector<uint16_t>* t1, std::vector<uint16_t>* t2, int* nstates) {

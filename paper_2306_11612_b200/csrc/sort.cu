@@ -32,8 +32,8 @@ __global__ void hist_scan_kernel(const uint32_t* __restrict__ hist, uint32_t* __
   base[p * 256 + d] = s[d];
 }
 
-template <typename K>
-__global__ void __launch_bounds__(kBlock)
+template <typename K, bool IOTA>
+__global__ void __launch_bounds__(kBlock, 2)
 onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                 K* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
                 const uint32_t* __restrict__ digit_base, uint32_t* status, uint32_t* tile_ctr) {
@@ -62,7 +62,7 @@ onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
     int64_t idx = wbase + i * 32 + lane;
     bool ok = idx < n;
     key[i] = ok ? kin[idx] : (K)0;
-    val[i] = ok ? vin[idx] : 0u;
+    val[i] = ok ? (IOTA ? (uint32_t)idx : vin[idx]) : 0u;   // first pass: ids are implicit
   }
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -121,15 +121,24 @@ onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
   }
   // decoupled look-back of digit d over the preceding tiles
   if (tile > 0) {
+    // four predecessors per round trip; tile 0 always publishes an inclusive count
     uint32_t excl = 0;
     int64_t j = tile - 1;
-    while (true) {
-      volatile uint32_t* sp = status + j * 256 + d;
-      uint32_t s = *sp;
-      while ((s >> 30) == 0) s = *sp;
-      excl += s & kSortMask;
-      if ((s >> 30) == 2) break;
-      --j;
+    bool done = false;
+    while (!done) {
+      uint32_t sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        sv[u] = j - u >= 0 ? *(volatile uint32_t*)(status + (j - u) * 256 + d) : (2u << 30);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!done) {
+          while ((sv[u] >> 30) == 0) sv[u] = *(volatile uint32_t*)(status + (j - u) * 256 + d);
+          excl += sv[u] & kSortMask;
+          done = (sv[u] >> 30) == 2;
+        }
+      }
+      j -= 4;
     }
     atomicExch(status + tile * 256 + d, kSortInc | (excl + cnt));
     s_scatter[d] = (int64_t)digit_base[d] + excl - start;
@@ -151,26 +160,42 @@ void launch_hist_scan(const uint32_t* hist, uint32_t* base, int passes, cudaStre
 }
 
 cudaError_t prepare_onesweep() {
-  cudaError_t e = cudaFuncSetAttribute(onesweep_kernel<uint32_t>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kSortTile * 8));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(onesweep_kernel<unsigned long long>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(kSortTile * 12));
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(onesweep_kernel<uint32_t, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSortTile * 8))))
+    return e;
+  if ((e = cudaFuncSetAttribute(onesweep_kernel<uint32_t, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSortTile * 8))))
+    return e;
+  if ((e = cudaFuncSetAttribute(onesweep_kernel<unsigned long long, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSortTile * 12))))
+    return e;
+  return cudaFuncSetAttribute(onesweep_kernel<unsigned long long, true>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSortTile * 12));
 }
 
 void launch_onesweep(const void* kin, const uint32_t* vin, void* kout, uint32_t* vout, int64_t n,
                      int key_bytes, int shift, const uint32_t* digit_base, uint32_t* status,
                      uint32_t* tile_ctr, cudaStream_t st) {
   int tiles = (int)((n + kSortTile - 1) / kSortTile);
-  if (key_bytes == 4)
-    onesweep_kernel<uint32_t><<<tiles, kBlock, kSortTile * 8, st>>>(
-        (const uint32_t*)kin, vin, (uint32_t*)kout, vout, n, shift, digit_base, status, tile_ctr);
-  else
-    onesweep_kernel<unsigned long long><<<tiles, kBlock, kSortTile * 12, st>>>(
-        (const unsigned long long*)kin, vin, (unsigned long long*)kout, vout, n, shift,
-        digit_base, status, tile_ctr);
+  const bool iota = vin == nullptr;
+  if (key_bytes == 4) {
+    if (iota)
+      onesweep_kernel<uint32_t, true><<<tiles, kBlock, kSortTile * 8, st>>>(
+          (const uint32_t*)kin, vin, (uint32_t*)kout, vout, n, shift, digit_base, status, tile_ctr);
+    else
+      onesweep_kernel<uint32_t, false><<<tiles, kBlock, kSortTile * 8, st>>>(
+          (const uint32_t*)kin, vin, (uint32_t*)kout, vout, n, shift, digit_base, status, tile_ctr);
+  } else {
+    if (iota)
+      onesweep_kernel<unsigned long long, true><<<tiles, kBlock, kSortTile * 12, st>>>(
+          (const unsigned long long*)kin, vin, (unsigned long long*)kout, vout, n, shift,
+          digit_base, status, tile_ctr);
+    else
+      onesweep_kernel<unsigned long long, false><<<tiles, kBlock, kSortTile * 12, st>>>(
+          (const unsigned long long*)kin, vin, (unsigned long long*)kout, vout, n, shift,
+          digit_base, status, tile_ctr);
+  }
 }
 
 }  // namespace dvl
