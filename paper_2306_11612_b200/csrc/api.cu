@@ -39,7 +39,8 @@ struct Dataset {
   // persistent TMA path (M <= 16)
   bool tma = false;
   TmaPlan plan{};
-  int grid = 0;                           // chunks = CTAs of both passes
+  int grid = 0;                           // pass-2 chunks = CTAs
+  int grid1 = 0;                          // pass-1 chunks = CTAs (look-back granularity)
   int planN = 0;                          // TF size the plan was made for
   int chunk_cap = 0;
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
@@ -300,26 +301,36 @@ void ensure_plan(dvl_ctx* ctx) {
   pl.stage_bytes =
       (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words()) + 127) & ~(size_t)127);
   pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
-  const size_t half = 100 * 1024, full = 205 * 1024;
+  // pass 2: 2 CTAs/SM when two stages fit in ~half an SM, else 1 CTA/SM
+  const size_t half = 100 * 1024, full = 205 * 1024, third = 66 * 1024;
   int stages = (int)((half - pl.tab_bytes) / pl.stage_bytes);
   if (pl.tab_bytes > half || stages < 2) stages = (int)((full - pl.tab_bytes) / pl.stage_bytes);
   pl.stages = std::min(stages, 4);
   if (pl.stages < 2) fail(ctx, DVL_E_INVAL, "TMA plan: stage does not fit in shared memory");
-  const int bps = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl);
+  // pass 1 (fewer registers): 3 CTAs/SM when two stages fit in a third of an SM
+  int stages1 = pl.tab_bytes < third ? (int)((third - pl.tab_bytes) / pl.stage_bytes) : 0;
+  pl.stages1 = stages1 >= 2 ? std::min(stages1, 4) : pl.stages;
+  pl.tpc1 = pl.tpc = 1;
+  const int bps = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 2);
+  const int bps1 = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 1);
   int G = std::min(d.tiles, ctx->num_sms * bps);
   pl.tpc = (d.tiles + G - 1) / G;
   G = (d.tiles + pl.tpc - 1) / pl.tpc;
-  if (G + 1 > d.chunk_cap) {
-    unsigned long long* cs = dalloc<unsigned long long>(ctx, G + 1);
-    unsigned long long* cp = dalloc<unsigned long long>(ctx, G);
+  int G1 = std::min(d.tiles, ctx->num_sms * bps1);
+  pl.tpc1 = (d.tiles + G1 - 1) / G1;
+  G1 = (d.tiles + pl.tpc1 - 1) / pl.tpc1;
+  if (G1 + 1 > d.chunk_cap) {
+    unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
+    unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);
     dfree(ctx, d.chunk_status);
     dfree(ctx, d.chunk_prefix);
     d.chunk_status = cs;
     d.chunk_prefix = cp;
-    d.chunk_cap = G + 1;
+    d.chunk_cap = G1 + 1;
   }
   d.plan = pl;
   d.grid = G;
+  d.grid1 = G1;
   d.planN = ctx->N;
 }
 
@@ -333,7 +344,7 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   tic(ctx, PH_MAXV);
   const bool exact = ctx->mode == DVL_MAXV_EXACT;
   launch_prologue(ctx, member, exact ? -1 : ctx->mode, d.tma ? d.chunk_status : nullptr,
-                  d.tma ? d.grid + 1 : 0);
+                  d.tma ? d.grid1 + 1 : 0);
   if (exact) {
     int grid = (int)(d.n_pad / ((int64_t)kBlock * d.items));
     launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);
@@ -342,8 +353,8 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   toc(ctx, PH_MAXV);
   tic(ctx, PH_WSCAN);
   if (d.tma) {
-    launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid, d.chunk_status,
-                              reinterpret_cast<uint32_t*>(d.chunk_status + d.grid), d.chunk_prefix,
+    launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid1, d.chunk_status,
+                              reinterpret_cast<uint32_t*>(d.chunk_status + d.grid1), d.chunk_prefix,
                               ctx->d_qtot, d.tile_meta, ctx->stream);
     CKLAUNCH();
     if (export_q) {

@@ -68,8 +68,10 @@ struct UpdParams {
 // Work split of the TMA-pipelined update kernels (host-computed).
 struct TmaPlan {
   int tiles;              // tiles of T = 256 * ITEMS cells
-  int tpc;                // tiles per chunk (one chunk per CTA)
-  int stages;             // shared-memory ring depth
+  int tpc;                // pass 2: tiles per chunk (one chunk per CTA)
+  int stages;             // pass 2: shared-memory ring depth
+  int tpc1;               // pass 1: tiles per chunk (its own occupancy)
+  int stages1;            // pass 1: ring depth
   uint32_t stage_bytes;   // M * T * 4 + T, rounded up to 128
   uint32_t tab_bytes;     // alpha table in shared memory (0: read through L1)
 };
