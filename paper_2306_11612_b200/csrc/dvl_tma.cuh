@@ -37,6 +37,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// the same wait, suspending the thread between polls for up to `ns` nanoseconds (it is woken
+// when the phase completes): for waits that are expected to be long (the producer waiting
+// for a free stage), so that the poll loop does not take issue slots from the consumers
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
 // L2 policy for streamed-once data
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
