@@ -2,6 +2,7 @@
 // stream ordering and per-phase CUDA-event timing.  Every compute step is a kernel from
 // hilbert.cu / sort.cu / build.cu / update.cu; this file only orchestrates them.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -96,6 +97,7 @@ struct dvl_ctx {
   int sort_passes = 0;
   int launches = 0;
   int num_sms = 148;
+  int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
 
   // sharding (dvl_set_global_bits / dvl_set_shard)
   int global_bits = 0;
@@ -252,6 +254,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.scale = pow2f(ctx->shift);
   p.shift = ctx->shift;
   p.offset = 0;
+  p.l2_keep = ctx->l2_keep;
   return p;
 }
 
@@ -307,9 +310,11 @@ void ensure_plan(dvl_ctx* ctx) {
   if (pl.tab_bytes > half || stages < 2) stages = (int)((full - pl.tab_bytes) / pl.stage_bytes);
   pl.stages = std::min(stages, 4);
   if (pl.stages < 2) fail(ctx, DVL_E_INVAL, "TMA plan: stage does not fit in shared memory");
-  // pass 1 (fewer registers): 3 CTAs/SM when two stages fit in a third of an SM
+  // pass 1 (and pass 2 for M <= 4, both compiled for 3 CTAs/SM): 3 CTAs/SM when two
+  // stages fit in a third of an SM
   int stages1 = pl.tab_bytes < third ? (int)((third - pl.tab_bytes) / pl.stage_bytes) : 0;
   pl.stages1 = stages1 >= 2 ? std::min(stages1, 4) : pl.stages;
+  if (d.M <= 4) pl.stages = pl.stages1;
   pl.tpc1 = pl.tpc = 1;
   const int bps = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 2);
   const int bps1 = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 1);
@@ -507,6 +512,7 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
       prepared = true;
     }
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    if (const char* e = getenv("DVL_L2_KEEP")) ctx->l2_keep = atoi(e);   // experiment knob
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dvl.h"
+
 namespace dvl {
 
 constexpr int kBlock = 256;            // threads of every streaming kernel
@@ -63,6 +65,7 @@ struct UpdParams {
   int shift;               // s
   uint64_t offset;         // global prefix before this device's cells (sharding, host part)
   const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
+  int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
 };
 
 // Work split of the TMA-pipelined update kernels (host-computed).
@@ -253,6 +256,30 @@ __device__ __forceinline__ void load_u8(const uint8_t* __restrict__ p, int (&v)[
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) v[j] = __ldg(p + j);
   }
+}
+
+// O14-O15: the vertex of one (member, pixel) from its count, min / max bits of t and the
+// 128-bit 2^-40 fixed-point sum of t (hi:lo words): mean = sum / count in double, rounded
+// to float, then the TF's RGBA at the mean.
+__device__ __forceinline__ dvl_vertex make_vertex(uint32_t cnt, uint32_t mn, uint32_t mx,
+                                                  unsigned long long shi, unsigned long long slo,
+                                                  const float4* tf, int N) {
+  dvl_vertex v;
+  v.count = cnt;
+  if (cnt) {
+    const double sum = ((double)shi * 18446744073709551616.0 + (double)slo) * kSumUnscale;
+    const float mean = (float)(sum / (double)cnt);
+    v.t_min = __uint_as_float(mn);
+    v.t_max = __uint_as_float(mx);
+    v.t_mean = mean;
+    v.r = sample_rgba(tf, N, mean, 0);
+    v.g = sample_rgba(tf, N, mean, 1);
+    v.b = sample_rgba(tf, N, mean, 2);
+    v.y = sample_rgba(tf, N, mean, 3);
+  } else {
+    v.t_min = v.t_max = v.t_mean = v.y = v.r = v.g = v.b = 0.0f;
+  }
+  return v;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {

@@ -589,42 +589,37 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
 }
 
 // ------------------------------------------------------------------------- epilogue
-__global__ void epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
-                                dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
-                                unsigned long long* bin_hi) {
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
-    unsigned long long lo = acc.lo[x], hi = acc.hi[x];
+// One warp per pixel x, lane m = member m (M <= 64: at most two rounds): the short
+// per-vertex work (a double division, four TF lookups) runs W*M-wide instead of W-wide.
+// Lane 0 reads and resets the pixel's cell range; each lane resets its member's partials.
+__global__ void __launch_bounds__(256)
+epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
+                dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
+                unsigned long long* bin_hi) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t x = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (x >= W) return;
+  unsigned long long lo = 0, hi = 0;
+  if (lane == 0) {
+    lo = acc.lo[x];
+    hi = acc.hi[x];
     acc.lo[x] = ~0ull;
     acc.hi[x] = 0ull;
     bin_lo[x] = lo;
     bin_hi[x] = hi;
-    const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
-    for (int m = 0; m < M; ++m) {
-      const int64_t k = (int64_t)m * W + x;
-      uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
-      unsigned long long sl = acc.slo[k], sh = acc.shi[k];
-      acc.tmin[k] = 0xffffffffu;
-      acc.tmax[k] = 0u;
-      acc.slo[k] = 0ull;
-      acc.shi[k] = 0ull;
-      dvl_vertex v;
-      v.count = cnt;
-      if (cnt) {
-        double sum = ((double)sh * 18446744073709551616.0 + (double)sl) * kSumUnscale;
-        float mean = (float)(sum / (double)cnt);
-        v.t_min = __uint_as_float(mn);
-        v.t_max = __uint_as_float(mx);
-        v.t_mean = mean;
-        const float4* tf = rgba + (int64_t)m * N;
-        v.r = sample_rgba(tf, N, mean, 0);
-        v.g = sample_rgba(tf, N, mean, 1);
-        v.b = sample_rgba(tf, N, mean, 2);
-        v.y = sample_rgba(tf, N, mean, 3);
-      } else {
-        v.t_min = v.t_max = v.t_mean = v.y = v.r = v.g = v.b = 0.0f;
-      }
-      out[k] = v;
-    }
+  }
+  lo = __shfl_sync(0xffffffffu, lo, 0);
+  hi = __shfl_sync(0xffffffffu, hi, 0);
+  const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
+  for (int m = lane; m < M; m += 32) {
+    const int64_t k = (int64_t)m * W + x;
+    const uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
+    const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
+    acc.tmin[k] = 0xffffffffu;
+    acc.tmax[k] = 0u;
+    acc.slo[k] = 0ull;
+    acc.shi[k] = 0ull;
+    out[k] = make_vertex(cnt, mn, mx, sh, sl, rgba + (int64_t)m * N, N);
   }
 }
 
@@ -645,7 +640,7 @@ __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
 void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                      cudaStream_t st) {
-  int grid = (int)((W + 255) / 256);
+  const int grid = (int)((W + 7) / 8);
   epilogue_kernel<<<grid, 256, 0, st>>>(acc, W, M, N, rgba, out, bin_lo, bin_hi);
 }
 
