@@ -98,6 +98,8 @@ struct dvl_ctx {
   int launches = 0;
   int num_sms = 148;
   int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
+  uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
+  int stages_override = 0;                // experiment: pass-2 ring depth
 
   // sharding (dvl_set_global_bits / dvl_set_shard)
   int global_bits = 0;
@@ -255,6 +257,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.shift = ctx->shift;
   p.offset = 0;
   p.l2_keep = ctx->l2_keep;
+  p.prod_sleep = ctx->prod_sleep;
   return p;
 }
 
@@ -304,19 +307,26 @@ void ensure_plan(dvl_ctx* ctx) {
   pl.stage_bytes =
       (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words()) + 127) & ~(size_t)127);
   pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
-  // pass 2: 2 CTAs/SM when two stages fit in ~half an SM, else 1 CTA/SM
-  const size_t half = 100 * 1024, full = 205 * 1024, third = 66 * 1024;
-  int stages = (int)((half - pl.tab_bytes) / pl.stage_bytes);
-  if (pl.tab_bytes > half || stages < 2) stages = (int)((full - pl.tab_bytes) / pl.stage_bytes);
-  pl.stages = std::min(stages, 4);
-  if (pl.stages < 2) fail(ctx, DVL_E_INVAL, "TMA plan: stage does not fit in shared memory");
-  // pass 1 (and pass 2 for M <= 4, both compiled for 3 CTAs/SM): 3 CTAs/SM when two
-  // stages fit in a third of an SM
-  int stages1 = pl.tab_bytes < third ? (int)((third - pl.tab_bytes) / pl.stage_bytes) : 0;
-  pl.stages1 = stages1 >= 2 ? std::min(stages1, 4) : pl.stages;
-  if (d.M <= 4) pl.stages = pl.stages1;
+  // Ring depths from per-CTA shared-memory budgets (228 KB per SM, ~3 KB per CTA reserved
+  // and static): 3 CTAs/SM (a third), 2 (a half), 1.  Pass 1 keeps the TF slope table in
+  // shared memory; pass 2 does not (only its boundary warps sample the TF, through L1), so
+  // its stages get all of the budget.  Pass 2 is compiled for 3 CTAs/SM only for M <= 4.
+  const size_t third = 74 * 1024, half = 110 * 1024, full = 220 * 1024;
+  auto fit = [&](size_t budget, size_t tab) -> int {
+    return tab < budget ? std::min(4, (int)((budget - tab) / pl.stage_bytes)) : 0;
+  };
+  auto depth = [&](size_t tab, bool three) -> int {
+    if (three && fit(third, tab) >= 2) return fit(third, tab);
+    if (fit(half, tab) >= 2) return fit(half, tab);
+    return fit(full, tab);
+  };
+  pl.stages1 = depth(pl.tab_bytes, true);
+  pl.stages = depth(0, d.M <= 4);
+  if (ctx->stages_override) pl.stages = ctx->stages_override;
+  if (pl.stages < 2 || pl.stages1 < 2)
+    fail(ctx, DVL_E_INVAL, "TMA plan: two stages do not fit in shared memory");
   pl.tpc1 = pl.tpc = 1;
-  const int bps = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 2);
+  const int bps = tma_blocks_per_sm(d.M, false, pl, 2);
   const int bps1 = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 1);
   int G = std::min(d.tiles, ctx->num_sms * bps);
   pl.tpc = (d.tiles + G - 1) / G;
@@ -363,7 +373,7 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
                               ctx->d_qtot, d.tile_meta, ctx->stream);
     CKLAUNCH();
     if (export_q) {
-      launch_bin_reduce_tma(d.plan.tab_bytes > 0, true, p, d.plan, d.grid, d.chunk_prefix,
+      launch_bin_reduce_tma(false, true, p, d.plan, d.grid, d.chunk_prefix,
                             ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, d.tile_meta, ctx->stream);
       CKLAUNCH();
     }
@@ -512,7 +522,9 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
       prepared = true;
     }
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    if (const char* e = getenv("DVL_L2_KEEP")) ctx->l2_keep = atoi(e);   // experiment knob
+    if (const char* e = getenv("DVL_L2_KEEP")) ctx->l2_keep = atoi(e);   // experiment knobs
+    if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
+    if (const char* e = getenv("DVL_STAGES2")) ctx->stages_override = atoi(e);
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
@@ -916,7 +928,7 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     Acc a = ctx->acc;
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
+      launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
                             ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta,
                             ctx->stream);
     else
@@ -1049,7 +1061,7 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     Acc a = ctx->acc;
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_bin_reduce_tma(d.plan.tab_bytes > 0, false, p, d.plan, d.grid, d.chunk_prefix,
+      launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
                             ctx->d_qtot_glob, W, a, ctx->cell_offset, ctx->d_err, nullptr,
                             d.tile_meta, ctx->stream);
     else

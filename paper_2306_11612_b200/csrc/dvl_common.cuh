@@ -66,6 +66,7 @@ struct UpdParams {
   uint64_t offset;         // global prefix before this device's cells (sharding, host part)
   const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
   int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
+  uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
 };
 
 // Work split of the TMA-pipelined update kernels (host-computed).
