@@ -63,5 +63,7 @@ def build_library(force: bool = False, verbose: bool = False, extra: list[str] |
 
 
 if __name__ == "__main__":
-    print(build_library(force="--force" in sys.argv, verbose=True,
-                        extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else None))
+    extra = ["-Xptxas", "-v"] if "--ptxas" in sys.argv else []
+    extra += ["-D" + a[len("--define="):] for a in sys.argv if a.startswith("--define=")]
+    print(build_library(force="--force" in sys.argv or any(a.startswith("--define=") for a in sys.argv),
+                        verbose=True, extra=extra))

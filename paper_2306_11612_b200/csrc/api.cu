@@ -97,9 +97,11 @@ struct dvl_ctx {
   int sort_passes = 0;
   int launches = 0;
   int num_sms = 148;
+  int acc_par = 0;                        // which lo / hi copy the next call uses
   int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
-  int stages_override = 0;                // experiment: pass-2 ring depth
+  int stages_override = 0;
+  int dbg = 0;                // experiment: pass-2 ring depth
 
   // sharding (dvl_set_global_bits / dvl_set_shard)
   int global_bits = 0;
@@ -258,6 +260,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.offset = 0;
   p.l2_keep = ctx->l2_keep;
   p.prod_sleep = ctx->prod_sleep;
+  p.dbg = ctx->dbg;
   return p;
 }
 
@@ -387,6 +390,16 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   toc(ctx, PH_WSCAN);
 }
 
+// the accumulators of this call: lo / hi from the copy of the current parity
+Acc cur_acc(const dvl_ctx* ctx) {
+  Acc a = ctx->acc;
+  if (ctx->acc_par) {
+    std::swap(a.lo, a.lo2);
+    std::swap(a.hi, a.hi2);
+  }
+  return a;
+}
+
 void ensure_acc(dvl_ctx* ctx, uint32_t W) {
   const int M = ctx->ds.M;
   if (ctx->accW >= W && ctx->accM == M) return;
@@ -395,6 +408,8 @@ void ensure_acc(dvl_ctx* ctx, uint32_t W) {
   Acc a{};
   a.lo = dalloc<unsigned long long>(ctx, cap);
   a.hi = dalloc<unsigned long long>(ctx, cap);
+  a.lo2 = dalloc<unsigned long long>(ctx, cap);
+  a.hi2 = dalloc<unsigned long long>(ctx, cap);
   a.tmin = dalloc<uint32_t>(ctx, (size_t)cap * M);
   a.tmax = dalloc<uint32_t>(ctx, (size_t)cap * M);
   a.slo = dalloc<unsigned long long>(ctx, (size_t)cap * M);
@@ -404,6 +419,8 @@ void ensure_acc(dvl_ctx* ctx, uint32_t W) {
   unsigned long long* bhi = dalloc<unsigned long long>(ctx, cap);
   dfree(ctx, ctx->acc.lo);
   dfree(ctx, ctx->acc.hi);
+  dfree(ctx, ctx->acc.lo2);
+  dfree(ctx, ctx->acc.hi2);
   dfree(ctx, ctx->acc.tmin);
   dfree(ctx, ctx->acc.tmax);
   dfree(ctx, ctx->acc.slo);
@@ -412,6 +429,7 @@ void ensure_acc(dvl_ctx* ctx, uint32_t W) {
   dfree(ctx, ctx->d_bin_lo);
   dfree(ctx, ctx->d_bin_hi);
   ctx->acc = a;
+  ctx->acc_par = 0;
   ctx->d_out = out;
   ctx->d_bin_lo = blo;
   ctx->d_bin_hi = bhi;
@@ -525,6 +543,7 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     if (const char* e = getenv("DVL_L2_KEEP")) ctx->l2_keep = atoi(e);   // experiment knobs
     if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
     if (const char* e = getenv("DVL_STAGES2")) ctx->stages_override = atoi(e);
+    if (const char* e = getenv("DVL_DBG")) ctx->dbg = atoi(e);
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
@@ -925,12 +944,11 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     UpdParams p = upd_params(ctx);
     // the member planes are indexed m * W + x for this call (capacity >= W); the epilogue
     // restores the identity of every entry it reads, so all entries stay identity
-    Acc a = ctx->acc;
+    Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta,
-                            ctx->stream);
+                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
@@ -940,6 +958,7 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_EPI);
     launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
     CKLAUNCH();
+    ctx->acc_par ^= 1;   // this call's copy is restored by the next call's epilogue
     toc(ctx, PH_EPI);
     ctx->last_W = W;
     if (where == DVL_MEM_HOST) {
@@ -1058,7 +1077,7 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     CKLAUNCH();
     UpdParams p = upd_params(ctx);
     p.offset_dev = ctx->d_offset;
-    Acc a = ctx->acc;
+    Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
@@ -1270,3 +1289,8 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
 }
 
 }  // extern "C"
+
+// timing experiments: pass-2 phase clock sums (see update_tma.cu); not part of dvl.h
+extern "C" __attribute__((visibility("default"))) int dvl_debug_stats(unsigned long long* out) {
+  return dvl::debug_stats(out, true) == cudaSuccess ? 0 : 1;
+}

@@ -67,6 +67,7 @@ struct UpdParams {
   const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
   int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
   uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
+  int dbg;                 // timing experiments only: 1 skip pass-2 folds, 2 skip pass-1 weights
 };
 
 // Work split of the TMA-pipelined update kernels (host-computed).
@@ -88,6 +89,11 @@ struct Acc {
   uint32_t* tmax;            // M x W
   unsigned long long* slo;   // M x W: low word of the 128-bit sum of round(t_part * 2^48)
   unsigned long long* shi;   // M x W: high word
+  // the other copy of lo / hi: get_polylines alternates between the two, and its epilogue
+  // restores the identity of the copy the previous call used (the current copy is read by
+  // the M threads of each pixel, so it cannot be reset in the same kernel)
+  unsigned long long* lo2;
+  unsigned long long* hi2;
 };
 
 // ------------------------------------------------------------------ fp32 recipes

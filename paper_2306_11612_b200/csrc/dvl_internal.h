@@ -88,6 +88,7 @@ struct TmaPlan;
 cudaError_t prepare_tma_kernels();
 int tma_items_for(int M);
 size_t tma_smem(const TmaPlan& plan);
+cudaError_t debug_stats(unsigned long long* out8, bool reset);
 int tma_blocks_per_sm(int M, bool smem_tab, const TmaPlan& plan, int pass);
 int tma_meta_words();
 void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,

@@ -69,7 +69,7 @@ void launch_acc_export(const Acc& acc, uint32_t W, int M, long long* out, cudaSt
   acc_export_kernel<<<grid, 256, 0, st>>>(acc, W, M, out);
 }
 
-// as epilogue_kernel (one warp per pixel, lane m = member m), from the merged planes
+// as epilogue_kernel (one thread per (member, pixel), pixel fastest), from the merged planes
 __global__ void __launch_bounds__(256)
 epilogue_merged_kernel(const long long* __restrict__ merged, uint32_t W, int M, int N,
                        const float4* __restrict__ rgba, dvl_vertex* __restrict__ out,
@@ -78,33 +78,31 @@ epilogue_merged_kernel(const long long* __restrict__ merged, uint32_t W, int M, 
   const long long* mn = merged;
   const long long* mx = merged + W + MW;
   const long long* sm = merged + 2 * (W + MW);
-  const int lane = threadIdx.x & 31;
-  const uint32_t x = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (x >= W) return;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= MW) return;
+  const int m = (int)(k / W);
+  const uint32_t x = (uint32_t)(k - (int64_t)m * W);
   const unsigned long long lo = mn[x] == 0x7fffffffffffffffll ? ~0ull : (unsigned long long)mn[x];
   const unsigned long long hi = (unsigned long long)mx[x];
-  if (lane == 0) {
+  if (m == 0) {
     bin_lo[x] = lo;
     bin_hi[x] = hi;
   }
   const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
-  for (int m = lane; m < M; m += 32) {
-    const int64_t k = (int64_t)m * W + x;
-    // 128-bit sum from the three limbs (each < 2^48 after summing <= 2^16 shards)
-    const unsigned long long l0 = (unsigned long long)sm[k], l1 = (unsigned long long)sm[MW + k],
-                             l2 = (unsigned long long)sm[2 * MW + k];
-    const unsigned long long a = l0 + (l1 << 32);
-    const unsigned long long carry = (a < l0 ? 1ull : 0ull) + (l1 >> 32);
-    const unsigned long long hiw = l2 + carry;
-    out[k] = make_vertex(cnt, (uint32_t)mn[W + k], (uint32_t)mx[W + k], hiw, a,
-                         rgba + (int64_t)m * N, N);
-  }
+  // 128-bit sum from the three limbs (each < 2^48 after summing <= 2^16 shards)
+  const unsigned long long l0 = (unsigned long long)sm[k], l1 = (unsigned long long)sm[MW + k],
+                           l2 = (unsigned long long)sm[2 * MW + k];
+  const unsigned long long a = l0 + (l1 << 32);
+  const unsigned long long carry = (a < l0 ? 1ull : 0ull) + (l1 >> 32);
+  const unsigned long long hiw = l2 + carry;
+  out[k] = make_vertex(cnt, (uint32_t)mn[W + k], (uint32_t)mx[W + k], hiw, a,
+                       rgba + (int64_t)m * N, N);
 }
 
 void launch_epilogue_merged(const long long* merged, uint32_t W, int M, int N, const float4* rgba,
                             dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                             cudaStream_t st) {
-  const int grid = (int)((W + 7) / 8);
+  const int grid = (int)(((int64_t)M * W + 255) / 256);
   epilogue_merged_kernel<<<grid, 256, 0, st>>>(merged, W, M, N, rgba, out, bin_lo, bin_hi);
 }
 

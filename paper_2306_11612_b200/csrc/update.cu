@@ -589,38 +589,32 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
 }
 
 // ------------------------------------------------------------------------- epilogue
-// One warp per pixel x, lane m = member m (M <= 64: at most two rounds): the short
-// per-vertex work (a double division, four TF lookups) runs W*M-wide instead of W-wide.
-// Lane 0 reads and resets the pixel's cell range; each lane resets its member's partials.
+// One thread per (member m, pixel x), x fastest (coalesced): reads the pixel's cell range
+// (current copy), m = 0 writes the bin ranges and restores the identity of the other copy;
+// every thread restores the identity of its member partials.
 __global__ void __launch_bounds__(256)
 epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
                 dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
                 unsigned long long* bin_hi) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t x = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (x >= W) return;
-  unsigned long long lo = 0, hi = 0;
-  if (lane == 0) {
-    lo = acc.lo[x];
-    hi = acc.hi[x];
-    acc.lo[x] = ~0ull;
-    acc.hi[x] = 0ull;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)M * W) return;
+  const int m = (int)(k / W);
+  const uint32_t x = (uint32_t)(k - (int64_t)m * W);
+  const unsigned long long lo = acc.lo[x], hi = acc.hi[x];
+  if (m == 0) {
     bin_lo[x] = lo;
     bin_hi[x] = hi;
+    acc.lo2[x] = ~0ull;
+    acc.hi2[x] = 0ull;
   }
-  lo = __shfl_sync(0xffffffffu, lo, 0);
-  hi = __shfl_sync(0xffffffffu, hi, 0);
   const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
-  for (int m = lane; m < M; m += 32) {
-    const int64_t k = (int64_t)m * W + x;
-    const uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
-    const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
-    acc.tmin[k] = 0xffffffffu;
-    acc.tmax[k] = 0u;
-    acc.slo[k] = 0ull;
-    acc.shi[k] = 0ull;
-    out[k] = make_vertex(cnt, mn, mx, sh, sl, rgba + (int64_t)m * N, N);
-  }
+  const uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
+  const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
+  acc.tmin[k] = 0xffffffffu;
+  acc.tmax[k] = 0u;
+  acc.slo[k] = 0ull;
+  acc.shi[k] = 0ull;
+  out[k] = make_vertex(cnt, mn, mx, sh, sl, rgba + (int64_t)m * N, N);
 }
 
 __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
@@ -629,6 +623,8 @@ __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
     if (k < W) {
       acc.lo[k] = ~0ull;
       acc.hi[k] = 0ull;
+      acc.lo2[k] = ~0ull;
+      acc.hi2[k] = 0ull;
     }
     acc.tmin[k] = 0xffffffffu;
     acc.tmax[k] = 0u;
@@ -640,7 +636,7 @@ __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
 void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                      cudaStream_t st) {
-  const int grid = (int)((W + 7) / 8);
+  const int grid = (int)(((int64_t)M * W + 255) / 256);
   epilogue_kernel<<<grid, 256, 0, st>>>(acc, W, M, N, rgba, out, bin_lo, bin_hi);
 }
 

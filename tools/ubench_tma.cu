@@ -1,0 +1,135 @@
+// Microbenchmark: streaming read throughput of the TF-update passes' data layout (M member
+// rows of fp32 + one u8 level row, 1024-cell tiles) on B200, through
+//   (a) the passes' design: persistent CTAs, 1 producer thread issuing 1D bulk copies
+//       (cp.async.bulk + mbarrier complete_tx) into an S-stage ring, 8 consumer warps that
+//       wait "full", read the stage from shared memory, release "empty";
+//   (b) plain vectorised global loads (ld.global.v4, grid-stride), as the reference point.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o ubench_tma ubench_tma.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+constexpr int kCons = 256, kThreads = 288, kT = 1024, kM = 4;
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void wait_par(uint64_t* bar, uint32_t par) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
+               ::"r"(sa(bar)), "r"(par) : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads) tma_stream(const float* scal, const uint8_t* level, int64_t n_pad,
+                                                       int tiles, int tpc, float* sink) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t stage_bytes = kM * kT * 4 + kT;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&empty[s])), "r"(8));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int t0 = blockIdx.x * tpc, nt = max(0, min(t0 + tpc, tiles) - t0);
+  if (warp == 8) {
+    if ((tid & 31) != 0) return;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int s = 0, ph = 0;
+    for (int k = 0; k < nt; ++k) {
+      if (k >= S) wait_par(&empty[s], ph ^ 1);
+      unsigned char* st = smem + (size_t)s * stage_bytes;
+      const int64_t c0 = (int64_t)(t0 + k) * kT;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(stage_bytes) : "memory");
+      for (int m = 0; m < kM; ++m)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(sa(st + m * kT * 4)), "l"(scal + m * n_pad + c0), "r"(kT * 4), "r"(sa(&full[s])), "l"(pol) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                   ::"r"(sa(st + kM * kT * 4)), "l"(level + c0), "r"(kT), "r"(sa(&full[s])), "l"(pol) : "memory");
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+    return;
+  }
+  float acc = 0.0f;
+  int s = 0, ph = 0;
+  for (int k = 0; k < nt; ++k) {
+    wait_par(&full[s], ph);
+    const float4* st = reinterpret_cast<const float4*>(smem + (size_t)s * stage_bytes);
+#pragma unroll
+    for (int m = 0; m < kM; ++m) {
+      float4 v = st[m * (kT / 4) + tid];
+      acc += v.x + v.y + v.z + v.w;
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
+    if (++s == S) { s = 0; ph ^= 1; }
+  }
+  if (acc == 1234.5f) sink[0] = acc;
+}
+
+__global__ void ldg_stream(const float4* scal, const uint32_t* level, int64_t n4, int64_t n_pad4, float* sink) {
+  float acc = 0.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = __ldcs(scal + i), b = __ldcs(scal + n_pad4 + i), c = __ldcs(scal + 2 * n_pad4 + i),
+           d = __ldcs(scal + 3 * n_pad4 + i);
+    uint32_t l = __ldcs(level + i);
+    acc += a.x + b.y + c.z + d.w + (float)(l & 1);
+  }
+  if (acc == 1234.5f) sink[0] = acc;
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t n = 10905182, tiles = (n + kT - 1) / kT, n_pad = tiles * kT;
+  float* scal;
+  uint8_t* level;
+  float* sink;
+  cudaMalloc(&scal, sizeof(float) * kM * n_pad);
+  cudaMalloc(&level, n_pad);
+  cudaMalloc(&sink, 4);
+  cudaMemset(scal, 0, sizeof(float) * kM * n_pad);
+  cudaMemset(level, 0, n_pad);
+  char* flush;
+  const size_t fl = 256u << 20;
+  cudaMalloc(&flush, fl);
+  const double bytes = (double)n_pad * (kM * 4 + 1);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto time_it = [&](auto launch, const char* name) {
+    float best = 1e9f;
+    for (int r = 0; r < 6; ++r) {
+      cudaMemsetAsync(flush, r, fl);
+      cudaEventRecord(a);
+      launch();
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (r > 0 && ms < best) best = ms;
+    }
+    printf("%-40s %8.2f us  %7.1f GB/s  (err %s)\n", name, best * 1e3, bytes / (best * 1e-3) / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  const uint32_t stage_bytes = kM * kT * 4 + kT;
+#define RUN(S, CPS)                                                                              \
+  {                                                                                              \
+    cudaFuncSetAttribute(tma_stream<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * stage_bytes); \
+    int G = sms * CPS, tpc = (int)((tiles + G - 1) / G);                                         \
+    G = (int)((tiles + tpc - 1) / tpc);                                                          \
+    char nm[64];                                                                                 \
+    snprintf(nm, 64, "tma ring S=%d, %d CTA/SM", S, CPS);                                        \
+    time_it([&] { tma_stream<S><<<G, kThreads, S * stage_bytes>>>(scal, level, n_pad, (int)tiles, tpc, sink); }, nm); \
+  }
+  RUN(2, 3) RUN(3, 3) RUN(4, 3) RUN(4, 2) RUN(6, 2) RUN(8, 1) RUN(12, 1) RUN(2, 4) RUN(3, 4)
+  for (int bl : {1, 2, 4, 8}) {
+    char nm[64];
+    snprintf(nm, 64, "ldg v4, %d x 256-thread blocks/SM", bl);
+    time_it([&] { ldg_stream<<<sms * bl * 2, 256>>>((const float4*)scal, (const uint32_t*)level, n_pad / 4, n_pad / 4, sink); }, nm);
+  }
+  return 0;
+}
