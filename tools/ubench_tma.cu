@@ -20,11 +20,12 @@ __device__ __forceinline__ void wait_par(uint64_t* bar, uint32_t par) {
 
 template <int S>
 __global__ void __launch_bounds__(kThreads) tma_stream(const float* scal, const uint8_t* level, int64_t n_pad,
-                                                       int tiles, int tpc, float* sink) {
+                                                       int tiles, int tpc, float* sink, int mode,
+                                                       const unsigned long long* meta) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full[S], empty[S];
   const int tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t stage_bytes = kM * kT * 4 + kT;
+  const uint32_t stage_bytes = kM * kT * 4 + kT + 128;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&full[s])), "r"(1));
@@ -33,7 +34,13 @@ __global__ void __launch_bounds__(kThreads) tma_stream(const float* scal, const 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // mode 0: contiguous chunk of tpc tiles per CTA; mode 1: chunks of 8 tiles round-robin
   const int t0 = blockIdx.x * tpc, nt = max(0, min(t0 + tpc, tiles) - t0);
+  auto tile_of = [&](int k) -> int {
+    if (mode == 0) return t0 + k;
+    const int j = k / 8, r = k % 8;
+    return (blockIdx.x + j * gridDim.x) * 8 + r;
+  };
   if (warp == 8) {
     if ((tid & 31) != 0) return;
     uint64_t pol;
@@ -42,8 +49,13 @@ __global__ void __launch_bounds__(kThreads) tma_stream(const float* scal, const 
     for (int k = 0; k < nt; ++k) {
       if (k >= S) wait_par(&empty[s], ph ^ 1);
       unsigned char* st = smem + (size_t)s * stage_bytes;
-      const int64_t c0 = (int64_t)(t0 + k) * kT;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(stage_bytes) : "memory");
+      const int tt = tile_of(k);
+      if (tt >= tiles) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&full[s])) : "memory"); if (++s == S) { s = 0; ph ^= 1; } continue; }
+      const int64_t c0 = (int64_t)tt * kT;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(kM * kT * 4 + kT + (meta ? 80 : 0)) : "memory");
+      if (meta)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(sa(st + kM * kT * 4 + kT)), "l"(meta + (int64_t)tt * 10), "r"(80), "r"(sa(&full[s])), "l"(pol) : "memory");
       for (int m = 0; m < kM; ++m)
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                      ::"r"(sa(st + m * kT * 4)), "l"(scal + m * n_pad + c0), "r"(kT * 4), "r"(sa(&full[s])), "l"(pol) : "memory");
@@ -115,7 +127,10 @@ int main() {
     printf("%-40s %8.2f us  %7.1f GB/s  (err %s)\n", name, best * 1e3, bytes / (best * 1e-3) / 1e9,
            cudaGetErrorString(cudaGetLastError()));
   };
-  const uint32_t stage_bytes = kM * kT * 4 + kT;
+  const uint32_t stage_bytes = kM * kT * 4 + kT + 128;
+  unsigned long long* meta;
+  cudaMalloc(&meta, tiles * 80);
+  cudaMemset(meta, 0, tiles * 80);
 #define RUN(S, CPS)                                                                              \
   {                                                                                              \
     cudaFuncSetAttribute(tma_stream<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * stage_bytes); \
@@ -123,9 +138,13 @@ int main() {
     G = (int)((tiles + tpc - 1) / tpc);                                                          \
     char nm[64];                                                                                 \
     snprintf(nm, 64, "tma ring S=%d, %d CTA/SM", S, CPS);                                        \
-    time_it([&] { tma_stream<S><<<G, kThreads, S * stage_bytes>>>(scal, level, n_pad, (int)tiles, tpc, sink); }, nm); \
+    time_it([&] { tma_stream<S><<<G, kThreads, S * stage_bytes>>>(scal, level, n_pad, (int)tiles, tpc, sink, 0, nullptr); }, nm); \
+    snprintf(nm, 64, "  same, chunks of 8 round-robin");                                       \
+    time_it([&] { tma_stream<S><<<G, kThreads, S * stage_bytes>>>(scal, level, n_pad, (int)tiles, tpc, sink, 1, nullptr); }, nm); \
+    snprintf(nm, 64, "  same (contiguous) + 80 B meta copy per tile");                          \
+    time_it([&] { tma_stream<S><<<G, kThreads, S * stage_bytes>>>(scal, level, n_pad, (int)tiles, tpc, sink, 0, meta); }, nm); \
   }
-  RUN(2, 3) RUN(3, 3) RUN(4, 3) RUN(4, 2) RUN(6, 2) RUN(8, 1) RUN(12, 1) RUN(2, 4) RUN(3, 4)
+  RUN(3, 3) RUN(4, 3) RUN(6, 2)
   for (int bl : {1, 2, 4, 8}) {
     char nm[64];
     snprintf(nm, 64, "ldg v4, %d x 256-thread blocks/SM", bl);
