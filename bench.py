@@ -147,6 +147,22 @@ def emit(obj):
 
 
 # ----------------------------------------------------------------------- reference arm
+def workload_config(name, n, M, W, N, levels, bits, world, sharded, gbits):
+    """The `config` object of the JSON line (shared by both arms)."""
+    ci = CONFIG_INDEX[name]
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            desc = json.load(f)["configs"][ci]
+    except Exception:
+        desc = "synthetic AMR ensemble"
+    return {"workload": f"{name} (BASELINE configs[{ci}]): {desc}",
+            "n_cells": n, "members": M, "W": W, "tf_size": N, "levels": levels,
+            "bits": bits, "edits": "member 0, new random TF per step",
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"sharded-dp{world}" if sharded else "single",
+            "cells_per_gpu": n, "global_bits": gbits or bits}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -183,8 +199,8 @@ def run_reference(args, rank, world):
           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/u64",
           "data": "synthetic",
-          "config": {"workload": f"{args.config}: synthetic AMR ensemble, {n_full} cells, M={M}, W={W}",
-                     "members": M, "W": W},
+          "config": workload_config(args.config, n_full, M, W, 256, int(B.Lmax) + 1, int(B.b), 1,
+                                    False, None),
           "cpu_baseline": {"value": value, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
                            "sample": sample},
           "e2e": {"value": value, "unit": "Gcells/s", "h2d_bytes_per_step": 0,
@@ -392,12 +408,8 @@ def run_native(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32/u64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: synthetic 3-level AMR ensemble (BASELINE configs[1])",
-                   "n_cells": n, "members": M, "W": W, "tf_size": N, "levels": int(info["Lmax"]) + 1,
-                   "bits": info["bits"], "edits": "member 0, new random TF per step",
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"sharded-dp{world}" if sharded else "single",
-                   "cells_per_gpu": n, "global_bits": gbits or info["bits"]},
+        "config": workload_config(args.config, n, M, W, N, int(info["Lmax"]) + 1, info["bits"], world,
+                                  sharded, gbits),
         "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90))},
         "kernels_ms": per_kernel,
