@@ -329,8 +329,9 @@ def run_native(args, rank, world, local):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    kern = {"maxv_ms": 0.0, "weights_scan_ms": 0.0, "bin_reduce_ms": 0.0, "epilogue_ms": 0.0}
-    launches = 0
+    # the timed steps run back to back (no host sync, no per-kernel events inside them)
+    ctx.set_timing(False)
+    ctx.timings()                         # resets the launch counter
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             with torch.cuda.stream(stream):
@@ -339,14 +340,22 @@ def run_native(args, rank, world, local):
             ctx.update_tf(0, edits[args.warmup + k])
             polylines(W, out=out_d)
             evs[k][1].record(stream)
-            t_pl = ctx.timings()          # synchronises; counts the step's launches
-            launches += t_pl["launches"]
-            for key in kern:
-                kern[key] += t_pl[key]
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+    launches = ctx.timings()["launches"]   # kernels launched in the timed region
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
+    # per-kernel breakdown: the same steps again with the library's per-kernel events
+    ctx.set_timing(True)
+    kern = {"maxv_ms": 0.0, "weights_scan_ms": 0.0, "bin_reduce_ms": 0.0, "epilogue_ms": 0.0}
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xff)
+        ctx.update_tf(0, edits[args.warmup + k])
+        polylines(W, out=out_d)
+        t_pl = ctx.timings()              # synchronises
+        for key in kern:
+            kern[key] += t_pl[key]
     total_ms = sum(step_ms)
     if dist:
         t = torch.tensor([total_ms], device=dev)

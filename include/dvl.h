@@ -254,6 +254,10 @@ dvl_status dvl_get_bin_ranges(dvl_ctx *ctx, uint32_t W, uint64_t *lo, uint64_t *
 /* Per-phase CUDA-event times of the last calls (see dvl_timings). */
 dvl_status dvl_get_timings(dvl_ctx *ctx, dvl_timings *t);
 
+/* Switch the per-kernel CUDA events of DVL_FLAG_TIMING on (enable != 0) or off, e.g. to time
+ * a sequence of calls without the event records between its kernels.  Errors: INVAL. */
+dvl_status dvl_set_timing(dvl_ctx *ctx, int enable);
+
 /* The context's CUDA stream (cudaStream_t), for callers that enqueue work around it. */
 void *dvl_stream(dvl_ctx *ctx);
 

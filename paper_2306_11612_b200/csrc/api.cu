@@ -76,9 +76,10 @@ struct dvl_ctx {
   unsigned long long* d_qtot = nullptr;
   uint32_t* d_ctr1 = nullptr;
   uint32_t* d_err = nullptr;
-  float* h_stage = nullptr;          // pinned + mapped: one TF (N x 4 floats)
+  float* h_stage = nullptr;          // pinned + mapped: two TF buffers (kMaxN x 4 floats each)
   float* d_hstage = nullptr;         // its device alias (read by the prologue kernel)
-  cudaEvent_t stage_ev = nullptr;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // prologue done with staging buffer i
+  int stage_par = 0;
   uint16_t* d_t1 = nullptr;
   uint16_t* d_t2 = nullptr;
   int nstates = 0;
@@ -284,18 +285,21 @@ void upload_domains(dvl_ctx* ctx) {
 
 // Put one N x 4 TF into the pinned, mapped staging buffer (after the previous reader of the
 // buffer has finished); the prologue kernel reads it over PCIe.
+// Two buffers alternate, so the host waits for the prologue before the previous one (not the
+// previous one itself) and can enqueue an edit while the GPU still runs the last.
 void stage_tf(dvl_ctx* ctx, const float* rgba, int N) {
-  CK(cudaEventSynchronize(ctx->stage_ev));
-  memcpy(ctx->h_stage, rgba, sizeof(float) * 4 * N);
+  ctx->stage_par ^= 1;
+  CK(cudaEventSynchronize(ctx->stage_ev[ctx->stage_par]));
+  memcpy(ctx->h_stage + (size_t)ctx->stage_par * 4 * kMaxN, rgba, sizeof(float) * 4 * N);
 }
 
 // The fused prologue: optional TF install of `member`, pass-1 state reset, max(V_h).
 void launch_prologue(dvl_ctx* ctx, int member, int mode, unsigned long long* zero, int zero_words) {
   Dataset& d = ctx->ds;
-  launch_tf_prologue(ctx->d_hstage, member, mode, d.M, ctx->N, d.d_rgba, d.d_tab, d.d_vmin,
+  launch_tf_prologue(ctx->d_hstage + (size_t)ctx->stage_par * 4 * kMaxN, member, mode, d.M, ctx->N, d.d_rgba, d.d_tab, d.d_vmin,
                      d.d_vmax, d.d_lo, d.d_inv, ctx->d_maxv, zero, zero_words, ctx->stream);
   CKLAUNCH();
-  if (member >= 0) CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
+  if (member >= 0) CK(cudaEventRecord(ctx->stage_ev[ctx->stage_par], ctx->stream));
 }
 
 // Work split of the TMA path for the current TF size: tile size from M, stage ring depth
@@ -550,10 +554,12 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     ctx->d_err = dalloc<uint32_t>(ctx, 1);
     ctx->d_offset = dalloc<unsigned long long>(ctx, 1);
     ctx->d_qtot_glob = dalloc<unsigned long long>(ctx, 1);
-    CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * 4 * kMaxN, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * 2 * 4 * kMaxN, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ctx->d_hstage, ctx->h_stage, 0));
-    CK(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(ctx->stage_ev, ctx->stream));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(ctx->stage_ev[i], ctx->stream));
+    }
     for (int i = 0; i < PH_N; ++i) {
       CK(cudaEventCreate(&ctx->ev[i][0]));
       CK(cudaEventCreate(&ctx->ev[i][1]));
@@ -586,7 +592,8 @@ void dvl_destroy(dvl_ctx* ctx) {
   for (void* p : ps) dfree(ctx, p);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
-  if (ctx->stage_ev) cudaEventDestroy(ctx->stage_ev);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
   for (int i = 0; i < PH_N; ++i)
     for (int j = 0; j < 2; ++j)
       if (ctx->ev[i][j]) cudaEventDestroy(ctx->ev[i][j]);
@@ -1266,6 +1273,15 @@ dvl_status dvl_get_bin_ranges(dvl_ctx* ctx, uint32_t W, uint64_t* lo, uint64_t* 
   } catch (Fail& f) {
     return f.s;
   }
+  return DVL_OK;
+}
+
+dvl_status dvl_set_timing(dvl_ctx* ctx, int enable) {
+  if (!ctx) return DVL_E_INVAL;
+  if (enable)
+    ctx->flags |= DVL_FLAG_TIMING;
+  else
+    ctx->flags &= ~DVL_FLAG_TIMING;
   return DVL_OK;
 }
 

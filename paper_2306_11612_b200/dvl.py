@@ -29,7 +29,7 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
            "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
            "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
-           "dvl_shard_finish"]
+           "dvl_shard_finish", "dvl_set_timing"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -302,6 +302,10 @@ class Context:
         self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(res), HOST),
                     "dvl_shard_finish")
         return res
+
+    def set_timing(self, enable: bool):
+        """Per-kernel CUDA events on / off (see dvl_set_timing)."""
+        self._check(self._lib.dvl_set_timing(self._h, int(bool(enable))), "dvl_set_timing")
 
     def timings(self) -> dict:
         t = _Timings()
