@@ -344,6 +344,8 @@ void ensure_plan(dvl_ctx* ctx) {
   if (G1 + 1 > d.chunk_cap) {
     unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
     unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);
+    // the last word holds pass 1's self-resetting chunk counters: zero once here
+    CK(cudaMemsetAsync(cs, 0, sizeof(unsigned long long) * (G1 + 1), ctx->stream));
     dfree(ctx, d.chunk_status);
     dfree(ctx, d.chunk_prefix);
     d.chunk_status = cs;
@@ -366,7 +368,7 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   tic(ctx, PH_MAXV);
   const bool exact = ctx->mode == DVL_MAXV_EXACT;
   launch_prologue(ctx, member, exact ? -1 : ctx->mode, d.tma ? d.chunk_status : nullptr,
-                  d.tma ? d.grid1 + 1 : 0);
+                  d.tma ? d.grid1 : 0);
   if (exact) {
     int grid = (int)(d.n_pad / ((int64_t)kBlock * d.items));
     launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);

@@ -52,6 +52,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
       : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel of the stream be scheduled now (its
+// CTAs run up to their pdl_wait), and wait until the previous kernel has completed and its
+// memory operations are visible.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // L2 policy for streamed-once data
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;

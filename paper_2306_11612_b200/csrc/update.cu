@@ -115,6 +115,9 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
                    const float* __restrict__ vmin, const float* __restrict__ vmax,
                    const float* __restrict__ lo, const float* __restrict__ inv, float* maxv,
                    unsigned long long* zero, int zero_words) {
+  // let pass 1 be scheduled now: its producer streams the scalars meanwhile, its consumers
+  // wait for this kernel (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x;
   if (member >= 0) {
     float4* rgba = rgba_all + (int64_t)member * N;
@@ -596,6 +599,7 @@ __global__ void __launch_bounds__(256)
 epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
                 dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
                 unsigned long long* bin_hi) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // launched dependent on pass 2
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (int64_t)M * W) return;
   const int m = (int)(k / W);
@@ -637,7 +641,16 @@ void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgb
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                      cudaStream_t st) {
   const int grid = (int)(((int64_t)M * W + 255) / 256);
-  epilogue_kernel<<<grid, 256, 0, st>>>(acc, W, M, N, rgba, out, bin_lo, bin_hi);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  (void)cudaLaunchKernelEx(&cfg, epilogue_kernel, acc, W, M, N, rgba, out, bin_lo, bin_hi);
 }
 
 void launch_acc_init(const Acc& acc, uint32_t W, int M, cudaStream_t st) {
