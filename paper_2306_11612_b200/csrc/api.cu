@@ -556,7 +556,7 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     ctx->d_err = dalloc<uint32_t>(ctx, 1);
     ctx->d_offset = dalloc<unsigned long long>(ctx, 1);
     ctx->d_qtot_glob = dalloc<unsigned long long>(ctx, 1);
-    CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * 2 * 4 * kMaxN, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&ctx->h_stage, sizeof(float) * (2 * 4 * kMaxN + 32), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ctx->d_hstage, ctx->h_stage, 0));
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
@@ -971,13 +971,16 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     toc(ctx, PH_EPI);
     ctx->last_W = W;
     if (where == DVL_MEM_HOST) {
+      // page-locked destination: one async DMA; pageable: the driver's staged copy
       CK(cudaMemcpyAsync(out, ctx->d_out, sizeof(dvl_vertex) * (size_t)W * d.M,
                          cudaMemcpyDeviceToHost, ctx->stream));
     }
     if (where == DVL_MEM_HOST || maybe_degenerate(ctx)) {
-      uint32_t herr = 0;
-      CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      // the error word through the context's pinned staging (an async copy, one sync)
+      uint32_t* herr_p = reinterpret_cast<uint32_t*>(ctx->h_stage + 2 * 4 * kMaxN);
+      CK(cudaMemcpyAsync(herr_p, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
+      const uint32_t herr = *herr_p;
       if (herr & kErrDegenerate) {
         CK(cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
         ctx->last_W = 0;
