@@ -46,7 +46,7 @@ struct Dataset {
   int chunk_cap = 0;
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
   unsigned long long* chunk_prefix = nullptr;   // grid
-  unsigned long long* tile_meta = nullptr;      // tiles x tma_meta_words(): pass-1 records
+  unsigned long long* tile_meta = nullptr;      // tiles x tma_meta_words(d.M): pass-1 records
 };
 
 }  // namespace
@@ -312,23 +312,17 @@ void ensure_plan(dvl_ctx* ctx) {
   const int T = kBlock * d.items;
   pl.tiles = d.tiles;
   pl.stage_bytes =
-      (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words()) + 127) & ~(size_t)127);
+      (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words(d.M)) + 127) & ~(size_t)127);
   pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
-  // Ring depths from per-CTA shared-memory budgets (228 KB per SM, ~3 KB per CTA reserved
-  // and static): 3 CTAs/SM (a third), 2 (a half), 1.  Pass 1 keeps the TF slope table in
-  // shared memory; pass 2 does not (only its boundary warps sample the TF, through L1), so
-  // its stages get all of the budget.  Pass 2 is compiled for 3 CTAs/SM only for M <= 4.
-  const size_t third = 74 * 1024, half = 110 * 1024, full = 220 * 1024;
-  auto fit = [&](size_t budget, size_t tab) -> int {
+  // One CTA per SM (Cfg in update_tma.cu): ring depth from the SM's shared memory (~220 KB
+  // usable with the static state), at most 4.  Pass 1 keeps the TF slope table in shared
+  // memory; pass 2 does not (only its boundary warps sample the TF, through L1).
+  const size_t budget = 225 * 1024;   // = the kernels' dynamic shared memory limit (prepare_tma_kernels)
+  auto fit = [&](size_t tab) -> int {
     return tab < budget ? std::min(4, (int)((budget - tab) / pl.stage_bytes)) : 0;
   };
-  auto depth = [&](size_t tab, bool three) -> int {
-    if (three && fit(third, tab) >= 2) return fit(third, tab);
-    if (fit(half, tab) >= 2) return fit(half, tab);
-    return fit(full, tab);
-  };
-  pl.stages1 = depth(pl.tab_bytes, true);
-  pl.stages = depth(0, d.M <= 4);
+  pl.stages1 = fit(pl.tab_bytes);
+  pl.stages = fit(0);
   if (ctx->stages_override) pl.stages = ctx->stages_override;
   if (pl.stages < 2 || pl.stages1 < 2)
     fail(ctx, DVL_E_INVAL, "TMA plan: two stages do not fit in shared memory");
@@ -370,7 +364,9 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   launch_prologue(ctx, member, exact ? -1 : ctx->mode, d.tma ? d.chunk_status : nullptr,
                   d.tma ? d.grid1 : 0);
   if (exact) {
-    int grid = (int)(d.n_pad / ((int64_t)kBlock * d.items));
+    // 4 cells per thread on the TMA layout (tiles of 4 * 256 * k cells), else the tile's
+    const int per = d.tma ? 4 : d.items;
+    int grid = (int)(d.n_pad / ((int64_t)kBlock * per));
     launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);
     CKLAUNCH();
   }
@@ -775,7 +771,7 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
     d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
     d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
-    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)d.tiles * tma_meta_words());
+    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)d.tiles * tma_meta_words(d.M));
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
   } catch (Fail& f) {
