@@ -46,7 +46,7 @@ struct Dataset {
   int chunk_cap = 0;
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
   unsigned long long* chunk_prefix = nullptr;   // grid
-  unsigned long long* tile_meta = nullptr;      // tiles x tma_meta_words(d.M): pass-1 records
+  unsigned long long* tile_meta = nullptr;      // n_pad / 128: pass-1 q sum of every warp tile
 };
 
 }  // namespace
@@ -309,32 +309,38 @@ void ensure_plan(dvl_ctx* ctx) {
   Dataset& d = ctx->ds;
   if (!d.tma || d.planN == ctx->N) return;
   TmaPlan pl{};
-  const int T = kBlock * d.items;
-  pl.tiles = d.tiles;
-  pl.stage_bytes =
-      (uint32_t)((((size_t)d.M * T * 4 + T + 8 * tma_meta_words(d.M)) + 127) & ~(size_t)127);
-  pl.tab_bytes = smem_tab_ok(ctx) ? (uint32_t)((((size_t)d.M * ctx->N * 8) + 127) & ~(size_t)127) : 0;
-  // One CTA per SM (Cfg in update_tma.cu): ring depth from the SM's shared memory (~220 KB
-  // usable with the static state), at most 4.  Pass 1 keeps the TF slope table in shared
-  // memory; pass 2 does not (only its boundary warps sample the TF, through L1).
-  const size_t budget = 225 * 1024;   // = the kernels' dynamic shared memory limit (prepare_tma_kernels)
-  auto fit = [&](size_t tab) -> int {
-    return tab < budget ? std::min(4, (int)((budget - tab) / pl.stage_bytes)) : 0;
+  const int64_t T1 = (int64_t)kBlock * d.items;        // pass-1 tile (n_pad is a multiple)
+  const int64_t T2 = tma_tile2_cells();                 // pass-2 tile
+  auto round128 = [](size_t b) { return (uint32_t)((b + 127) & ~(size_t)127); };
+  pl.tiles1 = (int)(d.n_pad / T1);
+  pl.tiles = (int)(d.n_pad / T2);
+  pl.stage_bytes1 = round128((size_t)d.M * T1 * 4 + T1);
+  pl.stage_bytes = round128((size_t)d.M * T2 * 4 + T2 + 8 * (T2 / tma_warp_tile_cells()));
+  pl.tab_bytes = smem_tab_ok(ctx) ? round128((size_t)d.M * ctx->N * 8) : 0;
+  // Ring depths (at most 4) from per-CTA shared-memory budgets: pass 1 runs one CTA per SM
+  // (the whole budget, which is the kernels' dynamic shared-memory limit set in
+  // prepare_tma_kernels) with the TF slope table; pass 2 runs 3 / 2 / 1 CTAs per SM for
+  // M <= 4 / 8 / 16 and keeps no table (only its boundary warps sample the TF, through L1).
+  const size_t full = 225 * 1024, half = 110 * 1024, third = 74 * 1024;
+  auto fit = [&](size_t budget, size_t tab, uint32_t stage) -> int {
+    return tab < budget ? std::min(4, (int)((budget - tab) / stage)) : 0;
   };
-  pl.stages1 = fit(pl.tab_bytes);
-  pl.stages = fit(0);
+  pl.stages1 = fit(full, pl.tab_bytes, pl.stage_bytes1);
+  const size_t b2 = d.M <= 4 ? third : d.M <= 8 ? half : full;
+  pl.stages = fit(b2, 0, pl.stage_bytes);
+  if (pl.stages < 2) pl.stages = fit(full, 0, pl.stage_bytes);
   if (ctx->stages_override) pl.stages = ctx->stages_override;
   if (pl.stages < 2 || pl.stages1 < 2)
     fail(ctx, DVL_E_INVAL, "TMA plan: two stages do not fit in shared memory");
   pl.tpc1 = pl.tpc = 1;
   const int bps = tma_blocks_per_sm(d.M, false, pl, 2);
   const int bps1 = tma_blocks_per_sm(d.M, pl.tab_bytes > 0, pl, 1);
-  int G = std::min(d.tiles, ctx->num_sms * bps);
-  pl.tpc = (d.tiles + G - 1) / G;
-  G = (d.tiles + pl.tpc - 1) / pl.tpc;
-  int G1 = std::min(d.tiles, ctx->num_sms * bps1);
-  pl.tpc1 = (d.tiles + G1 - 1) / G1;
-  G1 = (d.tiles + pl.tpc1 - 1) / pl.tpc1;
+  int G = std::min(pl.tiles, ctx->num_sms * bps);
+  pl.tpc = (pl.tiles + G - 1) / G;
+  G = (pl.tiles + pl.tpc - 1) / pl.tpc;
+  int G1 = std::min(pl.tiles1, ctx->num_sms * bps1);
+  pl.tpc1 = (pl.tiles1 + G1 - 1) / G1;
+  G1 = (pl.tiles1 + pl.tpc1 - 1) / pl.tpc1;
   if (G1 + 1 > d.chunk_cap) {
     unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
     unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);
@@ -771,7 +777,7 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
     d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
     d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
-    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)d.tiles * tma_meta_words(d.M));
+    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
   } catch (Fail& f) {

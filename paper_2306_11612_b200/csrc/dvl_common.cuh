@@ -72,13 +72,17 @@ struct UpdParams {
 
 // Work split of the TMA-pipelined update kernels (host-computed).
 struct TmaPlan {
-  int tiles;              // tiles of T = 256 * ITEMS cells
+  // pass 2: tiles of 1024 cells (8 warps x 128), 3 / 2 / 1 CTAs per SM for M <= 4 / 8 / 16
+  int tiles;              // tiles of pass 2
   int tpc;                // pass 2: tiles per chunk (one chunk per CTA)
   int stages;             // pass 2: shared-memory ring depth
-  int tpc1;               // pass 1: tiles per chunk (its own occupancy)
-  int stages1;            // pass 1: ring depth
-  uint32_t stage_bytes;   // M * T * 4 + T, rounded up to 128
-  uint32_t tab_bytes;     // alpha table in shared memory (0: read through L1)
+  uint32_t stage_bytes;   // pass 2: M * T * 4 + T + its 8 warp sums, rounded up to 128
+  // pass 1: one CTA per SM, tiles of CW * 128 cells
+  int tiles1;
+  int tpc1;
+  int stages1;
+  uint32_t stage_bytes1;  // M * T1 * 4 + T1, rounded up to 128
+  uint32_t tab_bytes;     // pass 1: alpha table in shared memory (0: read through L1)
 };
 
 // Per-bin accumulators of U4 (integer-exact, combined with atomics in any order).
