@@ -341,6 +341,12 @@ void ensure_plan(dvl_ctx* ctx) {
   int G1 = std::min(pl.tiles1, ctx->num_sms * bps1);
   pl.tpc1 = (pl.tiles1 + G1 - 1) / G1;
   G1 = (pl.tiles1 + pl.tpc1 - 1) / pl.tpc1;
+  // pass-1 tile order for L2 reuse by pass 2 (l2_keep: pass 1 leaves its reads in L2)
+  pl.order1 = 0;
+  if (ctx->l2_keep) {
+    const int64_t c2 = (int64_t)pl.tpc * T2;           // cells of a pass-2 chunk
+    pl.order1 = (c2 % T1 == 0 && (pl.tpc1 * T1) % c2 == 0) ? (int)(c2 / T1) : -1;
+  }
   if (G1 + 1 > d.chunk_cap) {
     unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
     unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);

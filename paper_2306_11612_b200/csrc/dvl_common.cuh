@@ -83,6 +83,8 @@ struct TmaPlan {
   int stages1;
   uint32_t stage_bytes1;  // M * T1 * 4 + T1, rounded up to 128
   uint32_t tab_bytes;     // pass 1: alpha table in shared memory (0: read through L1)
+  int order1;             // pass 1 tile order: 0 in order; k > 0: its chunk is k-tile groups
+                          // (one per pass-2 chunk) walked backwards in lockstep; -1 backwards
 };
 
 // Per-bin accumulators of U4 (integer-exact, combined with atomics in any order).
