@@ -147,7 +147,7 @@ def emit(obj):
 
 
 # ----------------------------------------------------------------------- reference arm
-def workload_config(name, n, M, W, N, levels, bits, world, sharded, gbits):
+def workload_config(name, n, M, W, N, levels, bits, world, sharded, gbits, n_per_gpu=None):
     """The `config` object of the JSON line (shared by both arms)."""
     ci = CONFIG_INDEX[name]
     try:
@@ -160,7 +160,7 @@ def workload_config(name, n, M, W, N, levels, bits, world, sharded, gbits):
             "bits": bits, "edits": "member 0, new random TF per step",
             "l2": "flushed (256 MiB write) before every timed step",
             "parallelism": f"sharded-dp{world}" if sharded else "single",
-            "cells_per_gpu": n, "global_bits": gbits or bits}
+            "cells_per_gpu": n_per_gpu or n, "global_bits": gbits or bits}
 
 
 def run_reference(args, rank, world):
@@ -272,18 +272,46 @@ def run_native(args, rank, world, local):
     lower_d = torch.from_numpy(c["lower"].view(np.int32)).to(dev)
     level_d = torch.from_numpy(c["level"]).to(dev)
     scal_d = torch.from_numpy(c["scal"]).to(dev)
+    n_global = n * world
+    if sharded:
+        # the build's input is a round-robin slice of the global generator order (untimed
+        # setup), so the distributed sample sort really moves cells between the ranks
+        from paper_2306_11612_b200 import dist_build
+        coll = dist_build.TorchCollectives()
+        dst = torch.arange(n, device=dev) % world
+        order = torch.argsort(dst, stable=True)
+        cnt = torch.bincount(dst, minlength=world)
+        allc = torch.stack(coll.all_gather(cnt))
+        sendc, recvc = cnt.tolist(), allc[:, rank].tolist()
+        lower_d = coll.all_to_all(lower_d.reshape(-1, 3)[order], sendc, recvc)
+        level_d = coll.all_to_all(level_d[order], sendc, recvc)
+        scal_d = coll.all_to_all(scal_d[:, order].t().contiguous(), sendc, recvc).t().contiguous()
     torch.cuda.synchronize()
 
     # ---- build (device-resident inputs), timed separately
     build_ms, phase = [], []
     for r in range(args.build_reps + 1):
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        ctx.build(lower_d, level_d, scal_d)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        if sharded:
+            # distributed build: local sort, sample sort exchange over NCCL, local sort of
+            # the received key range (host-synchronising collectives: wall clock, max over
+            # ranks)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dinfo = dist_build.distributed_build(ctx, lower_d, level_d, scal_d, coll)
+            torch.cuda.synchronize()
+            t = torch.tensor([1e3 * (time.perf_counter() - t0)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_b = float(t.item())
+        else:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            ctx.build(lower_d, level_d, scal_d)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms_b = ev0.elapsed_time(ev1)
         if r > 0:
-            build_ms.append(ev0.elapsed_time(ev1))
+            build_ms.append(ms_b)
             phase.append(ctx.timings())
     info = ctx.info()
     domain = c["domain"]
@@ -291,8 +319,7 @@ def run_native(args, rank, world, local):
     if sharded:
         from paper_2306_11612_b200.shard import ShardedContext
         sc = ShardedContext(ctx)
-        fin = np.where(np.isfinite(c["scal"]), c["scal"], np.nan)
-        sc.describe(n, int(info["Lmax"]), np.nanmin(fin, axis=1), np.nanmax(fin, axis=1))
+        n = int(dinfo["n_local"])          # this rank's cells after the exchange
         if domain is not None:   # shared domain: union over all ranks
             d = torch.tensor(domain, device=dev)
             lo_, hi_ = d[:, 0].contiguous(), d[:, 1].contiguous()
@@ -362,7 +389,7 @@ def run_native(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * n / (ms_per_step / 1e3) / 1e9
+    value = n_global / (ms_per_step / 1e3) / 1e9
 
     # ---- end-to-end through the public API with host buffers (TF H2D, vertices D2H)
     # the vertices land in page-locked host memory (one async DMA); the TF goes in through
@@ -384,7 +411,7 @@ def run_native(args, rank, world, local):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    assert res["count"].sum() >= n
+    assert res["count"][0].sum() >= n_global, (int(res["count"][0].sum()), n_global)
     if sharded:
         dist.barrier()
 
@@ -422,15 +449,15 @@ def run_native(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32/u64", "data": "synthetic",
-        "config": workload_config(args.config, n, M, W, N, int(info["Lmax"]) + 1, info["bits"], world,
-                                  sharded, gbits),
+        "config": workload_config(args.config, n_global, M, W, N, int(info["Lmax"]) + 1, info["bits"], world,
+                                  sharded, gbits, n_per_gpu=n_global // world),
         "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90))},
         "kernels_ms": per_kernel,
         "update_kernels_hbm_gbs": pass_bytes / (update_kernels_ms / 1e3) / 1e9,
         "build": {"ms": statistics.median(build_ms), "hilbert_sort_ms": bphase["encode_ms"] + bphase["sort_ms"],
                   **bphase, "sort_passes": phase[-1]["sort_passes"], "reps": len(build_ms)},
-        "e2e": {"value": world * n / (e2e_ms / 1e3) / 1e9, "unit": "Gcells/s", "ms_per_step": e2e_ms,
+        "e2e": {"value": n_global / (e2e_ms / 1e3) / 1e9, "unit": "Gcells/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": N * 16, "d2h_bytes_per_step": M * W * 32},
         "roofline": roof,
         "cpu_baseline": cpu,

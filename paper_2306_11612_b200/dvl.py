@@ -240,16 +240,34 @@ class Context:
         self._check(self._lib.dvl_info(self._h, ctypes.byref(i)), "dvl_info")
         return {k: getattr(i, k) for k, _ in _Info._fields_ if k != "reserved"}
 
-    def get_sorted(self):
-        codes = np.empty(self.n, np.uint64)
-        ids = np.empty(self.n, np.uint64)
-        self._check(self._lib.dvl_get_sorted(self._h, _ptr(codes), _ptr(ids), HOST), "dvl_get_sorted")
+    def get_sorted(self, device: bool = False):
+        """Sorted Hilbert codes and the input ids of the sorted cells (n x u64 each); numpy,
+        or torch CUDA int64 tensors with device=True."""
+        if device:
+            import torch
+            codes = torch.empty(self.n, dtype=torch.int64, device="cuda")
+            ids = torch.empty(self.n, dtype=torch.int64, device="cuda")
+            where = DEVICE
+        else:
+            codes = np.empty(self.n, np.uint64)
+            ids = np.empty(self.n, np.uint64)
+            where = HOST
+        self._check(self._lib.dvl_get_sorted(self._h, _ptr(codes), _ptr(ids), where), "dvl_get_sorted")
         return codes, ids
 
-    def get_sorted_data(self):
-        lv = np.empty(self.n, np.uint8)
-        sc = np.empty((self.M, self.n), np.float32)
-        self._check(self._lib.dvl_get_sorted_data(self._h, _ptr(lv), _ptr(sc), HOST),
+    def get_sorted_data(self, device: bool = False):
+        """Levels (n u8) and member scalars (M x n f32) in curve order (numpy, or torch CUDA
+        tensors with device=True)."""
+        if device:
+            import torch
+            lv = torch.empty(self.n, dtype=torch.uint8, device="cuda")
+            sc = torch.empty((self.M, self.n), dtype=torch.float32, device="cuda")
+            where = DEVICE
+        else:
+            lv = np.empty(self.n, np.uint8)
+            sc = np.empty((self.M, self.n), np.float32)
+            where = HOST
+        self._check(self._lib.dvl_get_sorted_data(self._h, _ptr(lv), _ptr(sc), where),
                     "dvl_get_sorted_data")
         return lv, sc
 
@@ -298,7 +316,7 @@ class Context:
             self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(out), DEVICE),
                         "dvl_shard_finish")
             return out
-        res = np.empty((self.M, W), VERTEX_DTYPE)
+        res = np.empty((self.M, W), VERTEX_DTYPE) if out is None else out
         self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(res), HOST),
                     "dvl_shard_finish")
         return res
