@@ -185,7 +185,7 @@ dvl_status dvl_get_polylines(dvl_ctx *ctx, uint32_t W, dvl_vertex *out, dvl_mem 
 /* ---- sharding: one context per GPU, each holding a contiguous range of the global curve
  * order.  Only two things cross shards per TF edit: the scan offset (the
  * sum of the earlier shards' fixed-point weights) and the per-pixel accumulators, which
- * are integers and merge exactly with MIN / MAX / SUM collectives.  The caller runs the
+ * are integers and merge exactly with a MAX and a SUM collective.  The caller runs the
  * collectives (e.g. torch.distributed over NCCL); the library never links NCCL. ---------- */
 
 /* Hilbert bits of the whole dataset, used by the next dvl_build of this shard instead of
@@ -217,13 +217,16 @@ uint64_t dvl_shard_export_words(dvl_ctx *ctx, uint32_t W);
 
 /* Pass 2 of this shard (U3+U4) with the global scan offset and Qtot derived on the device
  * from totals_dev[nshards] (the gathered dvl_shard_total values, shard order), then export
- * of the per-pixel accumulators to export_dev (device, dvl_shard_export_words int64): MIN
- * plane, MAX plane, SUM plane (see csrc/shard.cu).  Asynchronous.  Errors: STATE, INVAL. */
+ * of the per-pixel accumulators to export_dev (device, dvl_shard_export_words int64): the
+ * negated MIN plane (-first cell, -tmin bits), the MAX plane (last cell, tmax bits) and the
+ * SUM plane (128-bit sums as three 32-bit limbs), see csrc/shard.cu.  Merge: element-wise
+ * MAX over the first 2 (W + M W) words, SUM over the rest.  Asynchronous.  Errors: STATE,
+ * INVAL. */
 dvl_status dvl_shard_reduce(dvl_ctx *ctx, uint32_t W, const uint64_t *totals_dev, int nshards,
                             int shard, int64_t *export_dev);
 
-/* U5 from the merged export planes (element-wise MIN / MAX / SUM over all shards of the
- * three planes): out = M x W vertices as dvl_get_polylines.  Host output synchronises.
+/* U5 from the merged export (element-wise MAX over all shards of the -MIN and MAX planes,
+ * SUM of the SUM plane): out = M x W vertices as dvl_get_polylines.  Host output synchronises.
  * Errors: STATE, INVAL, DEGENERATE (merged Qtot = 0, checked with host output). */
 dvl_status dvl_shard_finish(dvl_ctx *ctx, uint32_t W, const int64_t *merged_dev,
                             dvl_vertex *out, dvl_mem where);

@@ -2,13 +2,14 @@
 // contiguous range of the global curve order; only two global quantities cross shards:
 //   * the scan offset: the sum of the earlier shards' fixed-point weights (and Qtot), from
 //     the gathered shard totals (shard_offsets_kernel);
-//   * the per-pixel accumulators, exported as int64 planes a collective can combine with
-//     plain MIN / MAX / SUM (acc_export_kernel) and turned into vertices after the merge
-//     (epilogue_merged_kernel).
+//   * the per-pixel accumulators, exported as int64 planes that two collectives combine:
+//     one MAX over the first two planes (the minima are exported negated: min x =
+//     -max(-x)) and one SUM over the third (acc_export_kernel); turned into vertices after
+//     the merge (epilogue_merged_kernel).
 // Everything is integer, so the merged result is bit-identical to the unsharded one.
 //
 // Export layout (int64, W pixels, M members):
-//   MIN plane  [W + M W]: lo (first cell; none -> INT64_MAX), tmin bits (none -> 2^32 - 1)
+//   -MIN plane [W + M W]: -lo (first cell; none -> -INT64_MAX), -tmin bits (none -> -(2^32-1))
 //   MAX plane  [W + M W]: hi (last cell; none -> 0),       tmax bits (none -> 0)
 //   SUM plane  [3 M W]:   the 128-bit sum as three 32-bit limbs, limb-major
 #include <algorithm>
@@ -45,12 +46,12 @@ __global__ void acc_export_kernel(Acc acc, uint32_t W, int M, long long* __restr
        k += (int64_t)gridDim.x * blockDim.x) {
     if (k < W) {
       const unsigned long long lo = acc.lo[k], hi = acc.hi[k];
-      mn[k] = lo == ~0ull ? 0x7fffffffffffffffll : (long long)lo;
+      mn[k] = -(lo == ~0ull ? 0x7fffffffffffffffll : (long long)lo);
       mx[k] = (long long)hi;
       acc.lo[k] = ~0ull;
       acc.hi[k] = 0ull;
     }
-    mn[W + k] = (long long)acc.tmin[k];
+    mn[W + k] = -(long long)acc.tmin[k];
     mx[W + k] = (long long)acc.tmax[k];
     const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
     sm[k] = (long long)(sl & 0xffffffffull);
@@ -82,7 +83,8 @@ epilogue_merged_kernel(const long long* __restrict__ merged, uint32_t W, int M, 
   if (k >= MW) return;
   const int m = (int)(k / W);
   const uint32_t x = (uint32_t)(k - (int64_t)m * W);
-  const unsigned long long lo = mn[x] == 0x7fffffffffffffffll ? ~0ull : (unsigned long long)mn[x];
+  const long long lo_s = -mn[x];   // the plane holds -min
+  const unsigned long long lo = lo_s == 0x7fffffffffffffffll ? ~0ull : (unsigned long long)lo_s;
   const unsigned long long hi = (unsigned long long)mx[x];
   if (m == 0) {
     bin_lo[x] = lo;
@@ -95,7 +97,7 @@ epilogue_merged_kernel(const long long* __restrict__ merged, uint32_t W, int M, 
   const unsigned long long a = l0 + (l1 << 32);
   const unsigned long long carry = (a < l0 ? 1ull : 0ull) + (l1 >> 32);
   const unsigned long long hiw = l2 + carry;
-  out[k] = make_vertex(cnt, (uint32_t)mn[W + k], (uint32_t)mx[W + k], hiw, a,
+  out[k] = make_vertex(cnt, (uint32_t)(-mn[W + k]), (uint32_t)mx[W + k], hiw, a,
                        rgba + (int64_t)m * N, N);
 }
 

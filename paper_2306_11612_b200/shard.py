@@ -3,8 +3,9 @@ contiguous range of the global curve order.  Per edit the ranks exchange
 
   1. their fixed-point weight totals (all_gather of one u64 each): every shard derives its
      scan offset and the global Qtot on the device (dvl_shard_reduce);
-  2. the per-pixel accumulators as three int64 planes merged with all_reduce MIN, MAX and SUM
-     (integers: the merged result is bit-identical to the unsharded one).
+  2. the per-pixel accumulators as three int64 planes merged with two all_reduces: MAX over
+     the first two (the minima are exported negated) and SUM over the third (integers: the
+     merged result is bit-identical to the unsharded one).
 
 This module is plumbing only: the arithmetic of both steps runs in the library's kernels;
 here are the collectives (torch.distributed, NCCL on GPUs, gloo on CPU) and the buffer views.
@@ -15,7 +16,7 @@ import numpy as np
 
 
 def export_layout(W: int, M: int):
-    """Word offsets (start, stop) of the MIN, MAX and SUM planes of an accumulator export."""
+    """Word offsets (start, stop) of the -MIN, MAX and SUM planes of an accumulator export."""
     mw = W + M * W
     return (0, mw), (mw, 2 * mw), (2 * mw, 2 * mw + 3 * M * W)
 
@@ -36,11 +37,21 @@ def gather_totals(local_total, group=None):
 
 
 def merge_planes(mn, mx, sm, group=None):
-    """In-place element-wise merge of the three planes over all ranks."""
+    """In-place element-wise merge of plain MIN / MAX / SUM planes over all ranks (three
+    collectives; used by the CPU decomposition test)."""
     import torch.distributed as dist
     dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=group)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=group)
+
+
+def merge_export(buf, W: int, M: int, group=None):
+    """In-place merge of an accumulator export over all ranks: one MAX all_reduce over the
+    -MIN and MAX planes (contiguous), one SUM all_reduce over the SUM plane."""
+    import torch.distributed as dist
+    (_, b), (_, d), (e, f) = export_layout(W, M)
+    dist.all_reduce(buf[:d], op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(buf[e:f], op=dist.ReduceOp.SUM, group=group)
 
 
 def scan_offset(totals, rank: int):
@@ -90,5 +101,5 @@ class ShardedContext:
         with torch.cuda.stream(stream):
             totals = gather_totals(self._total, self.group)
             self.ctx.shard_reduce(W, totals, self.rank, buf)
-            merge_planes(*split_planes(buf, W, self.ctx.M), group=self.group)
+            merge_export(buf, W, self.ctx.M, group=self.group)
             return self.ctx.shard_finish(W, buf, out)

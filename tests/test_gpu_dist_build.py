@@ -101,7 +101,7 @@ def test_distributed_build_and_sharded_update(dvl, G):
         exports.append(buf)
     torch.cuda.synchronize()
     planes = [shard.split_planes(e, W, M) for e in exports]
-    merged = torch.cat([torch.stack([p[0] for p in planes]).min(0).values,
+    merged = torch.cat([torch.stack([p[0] for p in planes]).max(0).values,
                         torch.stack([p[1] for p in planes]).max(0).values,
                         torch.stack([p[2] for p in planes]).sum(0)])
     out = ctxs[0].shard_finish(W, merged)

@@ -60,7 +60,7 @@ def run_sharded(dvl, lower, level, scal, tfs, W, G, generic, B):
         exports.append(buf)
     torch.cuda.synchronize()
     planes = [shard.split_planes(e, W, B.M) for e in exports]
-    mn = torch.stack([p[0] for p in planes]).min(0).values
+    mn = torch.stack([p[0] for p in planes]).max(0).values
     mx = torch.stack([p[1] for p in planes]).max(0).values
     sm = torch.stack([p[2] for p in planes]).sum(0)
     merged = torch.cat([mn, mx, sm])
