@@ -47,6 +47,8 @@ struct Dataset {
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
   unsigned long long* chunk_prefix = nullptr;   // grid
   unsigned long long* tile_meta = nullptr;      // n_pad / 128: pass-1 q sum of every warp tile
+  unsigned long long* blist = nullptr;          // 2 x n_pad / 128: pass-2 boundary warp tiles
+  uint32_t* bctr = nullptr;                     // their count + done counter (self-resetting)
 };
 
 }  // namespace
@@ -188,7 +190,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
-                d.tile_meta};
+                d.tile_meta, d.blist, d.bctr};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -391,7 +393,8 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
     CKLAUNCH();
     if (export_q) {
       launch_bin_reduce_tma(false, true, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, d.tile_meta, ctx->stream);
+                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, d.tile_meta, d.blist, d.bctr, ctx->num_sms,
+                            ctx->stream);
       CKLAUNCH();
     }
   } else {
@@ -783,7 +786,12 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
     d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
     d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
-    if (d.tma) d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+    if (d.tma) {
+      d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+      d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
+      d.bctr = dalloc<uint32_t>(ctx, 2);
+      CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), ctx->stream));
+    }
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
   } catch (Fail& f) {
@@ -965,7 +973,8 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta, ctx->stream);
+                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta, d.blist, d.bctr, ctx->num_sms,
+                            ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
@@ -1102,7 +1111,8 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
                             ctx->d_qtot_glob, W, a, ctx->cell_offset, ctx->d_err, nullptr,
-                            d.tile_meta, ctx->stream);
+                            d.tile_meta, d.blist, d.bctr, ctx->num_sms,
+                            ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
