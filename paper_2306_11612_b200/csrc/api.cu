@@ -312,7 +312,7 @@ void ensure_plan(dvl_ctx* ctx) {
   if (!d.tma || d.planN == ctx->N) return;
   TmaPlan pl{};
   const int64_t T1 = (int64_t)kBlock * d.items;        // pass-1 tile (n_pad is a multiple)
-  const int64_t T2 = tma_tile2_cells();                 // pass-2 tile
+  const int64_t T2 = tma_tile2_cells(d.M);             // pass-2 tile
   auto round128 = [](size_t b) { return (uint32_t)((b + 127) & ~(size_t)127); };
   pl.tiles1 = (int)(d.n_pad / T1);
   pl.tiles = (int)(d.n_pad / T2);
@@ -328,7 +328,8 @@ void ensure_plan(dvl_ctx* ctx) {
     return tab < budget ? std::min(4, (int)((budget - tab) / stage)) : 0;
   };
   pl.stages1 = fit(full, pl.tab_bytes, pl.stage_bytes1);
-  const size_t b2 = d.M <= 4 ? third : d.M <= 8 ? half : full;
+  const int c2 = tma_pass2_ctas_per_sm(d.M);
+  const size_t b2 = c2 >= 3 ? third : c2 == 2 ? half : full;
   pl.stages = fit(b2, 0, pl.stage_bytes);
   if (pl.stages < 2) pl.stages = fit(full, 0, pl.stage_bytes);
   if (ctx->stages_override) pl.stages = ctx->stages_override;
