@@ -329,7 +329,7 @@ void ensure_plan(dvl_ctx* ctx) {
   };
   pl.stages1 = fit(full, pl.tab_bytes, pl.stage_bytes1);
   const int c2 = tma_pass2_ctas_per_sm(d.M);
-  const size_t b2 = c2 >= 3 ? third : c2 == 2 ? half : full;
+  const size_t b2 = c2 >= 4 ? 55 * 1024 : c2 == 3 ? third : c2 == 2 ? half : full;
   pl.stages = fit(b2, 0, pl.stage_bytes);
   if (pl.stages < 2) pl.stages = fit(full, 0, pl.stage_bytes);
   if (ctx->stages_override) pl.stages = ctx->stages_override;
