@@ -11,6 +11,7 @@
 //     runs of equal digits contiguously.
 #include "dvl_common.cuh"
 #include "dvl_internal.h"
+#include "dvl_tma.cuh"
 
 namespace dvl {
 
@@ -45,9 +46,14 @@ onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
   __shared__ int64_t s_scatter[256];
   __shared__ uint32_t s_wsum[kBlock / 32];
   __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_bar;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  if (tid == 0) {
+    s_tile = atomicAdd(tile_ctr, 1u);
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int i = tid; i < (kBlock / 32) * 256; i += kBlock) (&s_warp[0][0])[i] = 0;
   __syncthreads();
   const int64_t tile = s_tile;
@@ -57,12 +63,31 @@ onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
   K key[kSortItems];
   uint32_t val[kSortItems];
   uint32_t rank[kSortItems];
+  if (tile_base + kSortTile <= n) {
+    // a full tile: one bulk copy of its keys (and ids) into shared memory (the staging area
+    // of the scatter below, free until then), so that the ranking reads them at shared
+    // memory latency instead of waiting on each global load
+    if (tid == 0) {
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(&s_bar, kSortTile * (uint32_t)(sizeof(K) + (IOTA ? 0 : 4)));
+      tma_load_1d(s_keys, kin + tile_base, kSortTile * (uint32_t)sizeof(K), &s_bar, pol);
+      if (!IOTA) tma_load_1d(s_vals, vin + tile_base, kSortTile * 4u, &s_bar, pol);
+    }
+    mbar_wait(&s_bar, 0);
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    int64_t idx = wbase + i * 32 + lane;
-    bool ok = idx < n;
-    key[i] = ok ? kin[idx] : (K)0;
-    val[i] = ok ? (IOTA ? (uint32_t)idx : vin[idx]) : 0u;   // first pass: ids are implicit
+    for (int i = 0; i < kSortItems; ++i) {
+      const int l = warp * (32 * kSortItems) + i * 32 + lane;
+      key[i] = s_keys[l];
+      val[i] = IOTA ? (uint32_t)(tile_base + l) : s_vals[l];   // first pass: ids are implicit
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      int64_t idx = wbase + i * 32 + lane;
+      bool ok = idx < n;
+      key[i] = ok ? kin[idx] : (K)0;
+      val[i] = ok ? (IOTA ? (uint32_t)idx : vin[idx]) : 0u;
+    }
   }
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
