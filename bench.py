@@ -374,7 +374,8 @@ def run_native(args, rank, world, local):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     # per-kernel breakdown: the same steps again with the library's per-kernel events
     ctx.set_timing(True)
-    kern = {"maxv_ms": 0.0, "weights_scan_ms": 0.0, "bin_reduce_ms": 0.0, "epilogue_ms": 0.0}
+    kern = {"maxv_ms": 0.0, "weights_scan_ms": 0.0, "bin_reduce_ms": 0.0, "bin_boundary_ms": 0.0,
+            "epilogue_ms": 0.0}
     for k in range(args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xff)
@@ -460,6 +461,10 @@ def run_native(args, rank, world, local):
         "e2e": {"value": n_global / (e2e_ms / 1e3) / 1e9, "unit": "Gcells/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": N * 16, "d2h_bytes_per_step": M * W * 32},
         "roofline": roof,
+        "paper_context": {"value": 0.61, "unit": "Gcells/s", "gpu": "NVIDIA A6000",
+                          "workload": "Molecular Cloud, 35.8 M cells x 4 fields, 4 AMR levels",
+                          "derived_from": "Table 1 (PAPER.md lines 390-395): 58.6 ms per TF edit",
+                          "note": "context only: another GPU and dataset, not the target"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches,

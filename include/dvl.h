@@ -114,7 +114,9 @@ typedef struct {
 typedef struct {
     float ingest_ms, encode_ms, sort_ms, gather_ms;      /* build phases */
     float maxv_ms, weights_scan_ms;                      /* dvl_update_tf */
-    float bin_reduce_ms, epilogue_ms;                    /* dvl_get_polylines */
+    float bin_reduce_ms, epilogue_ms;                    /* dvl_get_polylines: pass 2 (the
+                                                            streaming part), epilogue */
+    float bin_boundary_ms;                               /* pass 2's boundary warp tiles */
     int32_t sort_passes;
     int32_t launches;     /* kernels launched since the previous dvl_get_timings call */
 } dvl_timings;

@@ -17,7 +17,8 @@ using namespace dvl;
 
 namespace {
 
-enum Phase { PH_INGEST, PH_ENCODE, PH_SORT, PH_GATHER, PH_MAXV, PH_WSCAN, PH_BREDUCE, PH_EPI, PH_N };
+enum Phase { PH_INGEST, PH_ENCODE, PH_SORT, PH_GATHER, PH_MAXV, PH_WSCAN, PH_BREDUCE, PH_EPI,
+             PH_BOUND, PH_N };
 
 struct Dataset {
   int64_t n = 0, n_pad = 0;
@@ -974,13 +975,20 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta, d.blist, d.bctr, ctx->num_sms,
-                            ctx->stream);
+                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta,
+                            d.blist, d.bctr, ctx->num_sms, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
+    if (d.tma) {   // the warp tiles that straddle pixels
+      tic(ctx, PH_BOUND);
+      launch_bin_boundary(p, ctx->d_qtot, W, a, ctx->cell_offset, d.blist, d.bctr, ctx->num_sms,
+                          ctx->stream);
+      CKLAUNCH();
+      toc(ctx, PH_BOUND);
+    }
     dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
     tic(ctx, PH_EPI);
     launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
@@ -1112,13 +1120,19 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     if (d.tma)
       launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
                             ctx->d_qtot_glob, W, a, ctx->cell_offset, ctx->d_err, nullptr,
-                            d.tile_meta, d.blist, d.bctr, ctx->num_sms,
-                            ctx->stream);
+                            d.tile_meta, d.blist, d.bctr, ctx->num_sms, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
+    if (d.tma) {
+      tic(ctx, PH_BOUND);
+      launch_bin_boundary(p, ctx->d_qtot_glob, W, a, ctx->cell_offset, d.blist, d.bctr,
+                          ctx->num_sms, ctx->stream);
+      CKLAUNCH();
+      toc(ctx, PH_BOUND);
+    }
     launch_acc_export(a, W, d.M, (long long*)export_dev, ctx->stream);
     CKLAUNCH();
   } catch (Fail& f) {
@@ -1316,7 +1330,8 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
     float* dst[PH_N] = {&t->ingest_ms, &t->encode_ms, &t->sort_ms, &t->gather_ms,
-                        &t->maxv_ms, &t->weights_scan_ms, &t->bin_reduce_ms, &t->epilogue_ms};
+                        &t->maxv_ms, &t->weights_scan_ms, &t->bin_reduce_ms, &t->epilogue_ms,
+                        &t->bin_boundary_ms};
     for (int i = 0; i < PH_N; ++i)
       if (ctx->ev_used[i]) CK(cudaEventElapsedTime(dst[i], ctx->ev[i][0], ctx->ev[i][1]));
     t->sort_passes = ctx->sort_passes;

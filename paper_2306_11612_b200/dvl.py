@@ -65,7 +65,7 @@ class _ShardInfo(ctypes.Structure):
 class _Timings(ctypes.Structure):
     _fields_ = [(k, ctypes.c_float) for k in ("ingest_ms", "encode_ms", "sort_ms", "gather_ms",
                                               "maxv_ms", "weights_scan_ms", "bin_reduce_ms",
-                                              "epilogue_ms")] + \
+                                              "epilogue_ms", "bin_boundary_ms")] + \
                [("sort_passes", ctypes.c_int32), ("launches", ctypes.c_int32)]
 
 
