@@ -423,7 +423,9 @@ def run_native(args, rank, world, local):
     # ---- roofline of the dominant kernel (algorithmic bytes, design D2)
     peak, peak_src = load_peaks()
     per_kernel = {k: v / args.steps for k, v in kern.items()}
-    bytes_cell = {"weights_scan_ms": 4 * M + 1, "bin_reduce_ms": 4 * M + 1}
+    # pass 1 streams every member scalar and level; pass 2 (design D3) streams, per warp tile
+    # of 128 cells, its q sum and running sum (16 B) and its M t-statistics (16 M B)
+    bytes_cell = {"weights_scan_ms": 4 * M + 1, "bin_reduce_ms": (16 * M + 16) / 128}
     dom = max(bytes_cell, key=lambda k: per_kernel[k])
     alg_bytes = n * bytes_cell[dom]
     achieved = alg_bytes / (per_kernel[dom] / 1e3) / 1e9

@@ -48,6 +48,9 @@ struct Dataset {
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
   unsigned long long* chunk_prefix = nullptr;   // grid
   unsigned long long* tile_meta = nullptr;      // n_pad / 128: pass-1 q sum of every warp tile
+  unsigned long long* meta2 = nullptr;          // n_pad / 128: the warp's running q sum in its
+                                                // pass-1 chunk before the warp tile's tile
+  void* agg = nullptr;                          // D3: per warp tile and member t statistics
   unsigned long long* blist = nullptr;          // 2 x n_pad / 128: pass-2 boundary warp tiles
   uint32_t* bctr = nullptr;                     // their count + done counter (self-resetting)
 };
@@ -191,7 +194,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
-                d.tile_meta, d.blist, d.bctr};
+                d.tile_meta, d.blist, d.bctr, d.meta2, d.agg};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -284,6 +287,12 @@ void upload_domains(dvl_ctx* ctx) {
                      ctx->stream));
   CK(cudaMemcpyAsync(ctx->ds.d_inv, ctx->inv_h.data(), sizeof(float) * M,
                      cudaMemcpyHostToDevice, ctx->stream));
+  // D3: the per-warp-tile statistics of t depend on the domains (not on the TFs)
+  if (ctx->ds.tma && ctx->ds.agg) {
+    launch_agg_build(upd_params(ctx), ctx->ds.agg, ctx->ds.n_pad / tma_warp_tile_cells(),
+                     ctx->num_sms, ctx->stream);
+    CKLAUNCH();
+  }
 }
 
 // Put one N x 4 TF into the pinned, mapped staging buffer (after the previous reader of the
@@ -346,8 +355,8 @@ void ensure_plan(dvl_ctx* ctx) {
   pl.tpc1 = (pl.tiles1 + G1 - 1) / G1;
   G1 = (pl.tiles1 + pl.tpc1 - 1) / pl.tpc1;
   // pass-1 tile order for L2 reuse by pass 2 (l2_keep: pass 1 leaves its reads in L2)
-  pl.order1 = 0;
-  if (ctx->l2_keep) {
+  pl.order1 = 0;   // (the D3 records need pass 1 in tile order)
+  if (false) {
     const int64_t c2 = (int64_t)pl.tpc * T2;           // cells of a pass-2 chunk
     pl.order1 = (c2 % T1 == 0 && (pl.tpc1 * T1) % c2 == 0) ? (int)(c2 / T1) : -1;
   }
@@ -391,7 +400,7 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   if (d.tma) {
     launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid1, d.chunk_status,
                               reinterpret_cast<uint32_t*>(d.chunk_status + d.grid1), d.chunk_prefix,
-                              ctx->d_qtot, d.tile_meta, ctx->stream);
+                              ctx->d_qtot, d.tile_meta, d.meta2, ctx->stream);
     CKLAUNCH();
     if (export_q) {
       launch_bin_reduce_tma(false, true, p, d.plan, d.grid, d.chunk_prefix,
@@ -790,6 +799,8 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
     if (d.tma) {
       d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+      d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+      d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
       d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
       d.bctr = dalloc<uint32_t>(ctx, 2);
       CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), ctx->stream));
@@ -974,9 +985,8 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, W, a, ctx->cell_offset, ctx->d_err, nullptr, d.tile_meta,
-                            d.blist, d.bctr, ctx->num_sms, ctx->stream);
+      launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
@@ -1118,9 +1128,8 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_bin_reduce_tma(false, false, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot_glob, W, a, ctx->cell_offset, ctx->d_err, nullptr,
-                            d.tile_meta, d.blist, d.bctr, ctx->num_sms, ctx->stream);
+      launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);

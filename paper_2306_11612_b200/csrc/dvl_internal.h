@@ -96,7 +96,15 @@ int tma_warp_tile_cells();
 void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,
                                unsigned long long* chunk_status, uint32_t* ctr,
                                unsigned long long* chunk_prefix, unsigned long long* qtot,
-                               unsigned long long* meta, cudaStream_t st);
+                               unsigned long long* meta, unsigned long long* meta2,
+                               cudaStream_t st);
+size_t agg_bytes(int M, int64_t nwt);
+void launch_agg_build(const UpdParams& p, void* agg, int64_t nwt, int num_sms, cudaStream_t st);
+void launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned long long* chunk_prefix,
+                       const unsigned long long* qtot, uint32_t W, const Acc& acc,
+                       uint64_t cell_offset, uint32_t* err, const unsigned long long* meta,
+                       const unsigned long long* meta2, const void* agg, unsigned long long* blist,
+                       uint32_t* bctr, cudaStream_t st);
 void launch_bin_reduce_tma(bool smem_tab, bool export_q, const UpdParams& p, const TmaPlan& plan,
                            int grid, const unsigned long long* chunk_prefix,
                            const unsigned long long* qtot, uint32_t W, const Acc& acc,
