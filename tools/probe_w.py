@@ -51,7 +51,7 @@ def main():
                 buf = (ctypes.c_ulonglong * (8 + 2048 + 4096))()
                 dvl.load().dvl_debug_stats(buf)
                 v = list(buf)
-                if it == 7:
+                if it == 7 and any(v[8:8 + 2048]):
                     cta = np.array(v[8:8 + 2048], dtype=np.uint64)
                     ts = np.array(v[8 + 2048:], dtype=np.int64).reshape(-1, 2)
                     cyc = (cta & np.uint64((1 << 40) - 1)).astype(np.int64)
