@@ -13,12 +13,12 @@ import re
 import sys
 
 # the kernels of one TF-update step (acc_init runs once per context / pixel count)
-UPDATE = ("tf_prologue_kernel", "maxv_exact_kernel", "weights_reduce_tma", "bin_reduce_tma",
-          "epilogue_kernel", "weights_scan_kernel", "bin_reduce_kernel")
+UPDATE = ("tf_prologue_kernel", "maxv_exact_kernel", "weights_reduce_tma", "agg_reduce",
+          "bin_boundary", "epilogue_kernel", "weights_scan_kernel", "bin_reduce_kernel")
 
 
 def short(name):
-    m = re.search(r"dvl::(\w+)", name)
+    m = re.search(r"dvl::(\w+)", name) or re.search(r"\b(agg_reduce|agg_build|bin_boundary|weights_reduce_tma|bin_reduce_tma)\b", name)
     if m:
         return m.group(1)
     m = re.match(r"(?:void )?([\w:]+)", name)
