@@ -32,7 +32,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 
 
 def short(name):
-    m = re.search(r"(weights_reduce_tma|bin_reduce_tma|\w+_kernel)", name)
+    m = re.search(r"(weights_reduce_tma|bin_reduce_tma|agg_reduce|agg_build|bin_boundary|\w+_kernel)", name)
     return m.group(1) if m else name[:40]
 
 
