@@ -221,7 +221,8 @@ uint64_t dvl_shard_export_words(dvl_ctx *ctx, uint32_t W);
  * from totals_dev[nshards] (the gathered dvl_shard_total values, shard order), then export
  * of the per-pixel accumulators to export_dev (device, dvl_shard_export_words int64): the
  * negated MIN plane (-first cell, -tmin bits), the MAX plane (last cell, tmax bits) and the
- * SUM plane (128-bit sums as three 32-bit limbs), see csrc/shard.cu.  Merge: element-wise
+ * SUM plane (128-bit sums as limbs of weight 2^0, 2^32, 2^64, each < 2^33), see
+ * csrc/shard.cu.  Merge: element-wise
  * MAX over the first 2 (W + M W) words, SUM over the rest.  Asynchronous.  Errors: STATE,
  * INVAL. */
 dvl_status dvl_shard_reduce(dvl_ctx *ctx, uint32_t W, const uint64_t *totals_dev, int nshards,

@@ -93,8 +93,8 @@ struct Acc {
   unsigned long long* hi;    // W: last cell (max)
   uint32_t* tmin;            // M x W: min of t bits (t >= 0, so bits order like values)
   uint32_t* tmax;            // M x W
-  unsigned long long* slo;   // M x W: low word of the 128-bit sum of round(t_part * 2^48)
-  unsigned long long* shi;   // M x W: high word
+  unsigned long long* slo;   // M x W: sum of the low 32-bit halves of the 2^-40 fixed-point adds
+  unsigned long long* shi;   // M x W: sum of the high halves (sum = slo + shi * 2^32, red_add_sum)
   // the other copy of lo / hi: get_polylines alternates between the two, and its epilogue
   // restores the identity of the copy the previous call used (the current copy is read by
   // the M threads of each pixel, so it cannot be reset in the same kernel)
@@ -311,11 +311,21 @@ __device__ __forceinline__ unsigned long long warp_incl_scan_u64(unsigned long l
 }
 
 // 128-bit atomic add of a u64 into (lo, hi) words: exact in any order.
-__device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned long long* hi,
-                                                unsigned long long v) {
+// The fixed-point sums are kept as two 64-bit counters, of the low and of the high 32-bit
+// halves of the added values (sum = slo + shi * 2^32): no carry to propagate, so both adds
+// are fire-and-forget reductions (no round trip to L2 for a returned value).  Exact while a
+// counter takes < 2^32 adds (one per flush of a warp or group: n < 2^38 cells).
+__device__ __forceinline__ void red_add_sum(unsigned long long* slo, unsigned long long* shi,
+                                            unsigned long long v) {
   if (v == 0) return;
-  unsigned long long old = atomicAdd(lo, v);
-  if (old + v < old) atomicAdd(hi, 1ull);
+  atomicAdd(slo, v & 0xffffffffull);
+  if (v >> 32) atomicAdd(shi, v >> 32);
+}
+// the 128-bit sum (hi:lo words) of the two counters
+__device__ __forceinline__ void sum_words(unsigned long long slo, unsigned long long shi,
+                                          unsigned long long& hw, unsigned long long& lw) {
+  lw = slo + (shi << 32);
+  hw = (shi >> 32) + (lw < slo ? 1ull : 0ull);
 }
 
 }  // namespace dvl

@@ -53,10 +53,11 @@ __global__ void acc_export_kernel(Acc acc, uint32_t W, int M, long long* __restr
     }
     mn[W + k] = -(long long)acc.tmin[k];
     mx[W + k] = (long long)acc.tmax[k];
+    // limbs of 2^0, 2^32, 2^64 (sum = slo + shi * 2^32; each limb < 2^33)
     const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
     sm[k] = (long long)(sl & 0xffffffffull);
-    sm[MW + k] = (long long)(sl >> 32);
-    sm[2 * MW + k] = (long long)sh;
+    sm[MW + k] = (long long)((sl >> 32) + (sh & 0xffffffffull));
+    sm[2 * MW + k] = (long long)(sh >> 32);
     acc.tmin[k] = 0xffffffffu;
     acc.tmax[k] = 0u;
     acc.slo[k] = 0ull;
@@ -91,7 +92,7 @@ epilogue_merged_kernel(const long long* __restrict__ merged, uint32_t W, int M, 
     bin_hi[x] = hi;
   }
   const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
-  // 128-bit sum from the three limbs (each < 2^48 after summing <= 2^16 shards)
+  // 128-bit sum from the three limbs (each < 2^49 after summing <= 2^16 shards)
   const unsigned long long l0 = (unsigned long long)sm[k], l1 = (unsigned long long)sm[MW + k],
                            l2 = (unsigned long long)sm[2 * MW + k];
   const unsigned long long a = l0 + (l1 << 32);

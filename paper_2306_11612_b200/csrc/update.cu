@@ -351,7 +351,7 @@ __device__ __forceinline__ void flush_member(const Acc& acc, uint32_t W, int m, 
   const int64_t k = (int64_t)m * W + x;
   atomicMin(acc.tmin + k, mn);
   atomicMax(acc.tmax + k, mx);
-  atomic_add_u128(acc.slo + k, acc.shi + k, __float2ull_rn(__fmul_rn(sum, kSumScale)));
+  red_add_sum(acc.slo + k, acc.shi + k, __float2ull_rn(__fmul_rn(sum, kSumScale)));
 }
 
 __device__ __forceinline__ void flush_range(const Acc& acc, int x, unsigned long long first,
@@ -492,7 +492,7 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
       const int64_t k = (int64_t)m * W + xt;
       atomicMin(acc.tmin + k, mn);
       atomicMax(acc.tmax + k, mx);
-      atomic_add_u128(acc.slo + k, acc.shi + k, fx);
+      red_add_sum(acc.slo + k, acc.shi + k, fx);
     }
     if (tid == 0) {
       const unsigned long long first = cell_offset + (unsigned long long)(tile * T);
@@ -531,7 +531,7 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
         const int64_t k = (int64_t)m * W + xw;
         atomicMin(acc.tmin + k, mn);
         atomicMax(acc.tmax + k, mx);
-        atomic_add_u128(acc.slo + k, acc.shi + k, fx);
+        red_add_sum(acc.slo + k, acc.shi + k, fx);
       }
     }
     // cell range of the warp: first valid cell of lane 0, last valid cell of the warp
@@ -613,7 +613,8 @@ epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rg
   }
   const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
   const uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
-  const unsigned long long sl = acc.slo[k], sh = acc.shi[k];
+  unsigned long long sl, sh;
+  sum_words(acc.slo[k], acc.shi[k], sh, sl);
   acc.tmin[k] = 0xffffffffu;
   acc.tmax[k] = 0u;
   acc.slo[k] = 0ull;

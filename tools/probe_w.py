@@ -77,8 +77,8 @@ def main():
                 bd = v[8 + 2048 + 4096 - 8:]
                 if it >= 3 and bd[5]:
                     ne = bd[5]
-                    print("  boundary per entry (kcycles): to-entry %.1f stage %.1f weights %.1f bins %.1f fold+flush %.1f | per warp total %.1f | entries %d" % (
-                        bd[0] / ne / 1e3, bd[1] / ne / 1e3, bd[2] / ne / 1e3, bd[3] / ne / 1e3, bd[4] / ne / 1e3, bd[7] / (2 * 148 * 8) / 1e3, ne))
+                    print("  boundary per entry (kcycles): to-entry %.1f stage %.1f weights %.1f bins %.1f fold+mid %.1f flush %.1f | per warp total %.1f | entries %d" % (
+                        bd[0] / ne / 1e3, bd[1] / ne / 1e3, bd[2] / ne / 1e3, bd[3] / ne / 1e3, bd[4] / ne / 1e3, bd[6] / ne / 1e3, bd[7] / (2 * 148 * 8) / 1e3, ne))
                 if it >= 3:
                     nw = max(v[5], 1)
                     print("  per warp (kcycles): prologue %.1f wait %.1f slow %.1f loop %.1f flush %.2f"
