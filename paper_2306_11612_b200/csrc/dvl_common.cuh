@@ -87,6 +87,30 @@ struct TmaPlan {
                           // (one per pass-2 chunk) walked backwards in lockstep; -1 backwards
 };
 
+// Division by the pixel count W of one get_polylines call (2 <= W <= 2^16) with a
+// multiply-high and shifts (Granlund and Montgomery, "Division by invariant integers using
+// multiplication", PLDI 1994, Fig. 4.1): exact for every 32-bit numerator.  Built on the host.
+struct WDiv {
+  uint32_t d, m, s;   // divisor, magic, l - 1 with l = ceil(log2 d) >= 1
+  static WDiv make(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    WDiv w;
+    w.d = d;
+    w.s = l - 1;
+    w.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    return w;
+  }
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    const uint32_t t = __umulhi(m, n);
+#else
+    const uint32_t t = (uint32_t)(((unsigned long long)m * n) >> 32);
+#endif
+    return (t + ((n - t) >> 1)) >> s;
+  }
+};
+
 // Per-bin accumulators of U4 (integer-exact, combined with atomics in any order).
 struct Acc {
   unsigned long long* lo;    // W: first cell (min)

@@ -81,7 +81,7 @@ def main():
                         bd[0] / ne / 1e3, bd[1] / ne / 1e3, bd[2] / ne / 1e3, bd[3] / ne / 1e3, bd[4] / ne / 1e3, bd[6] / ne / 1e3, bd[7] / (2 * 148 * 8) / 1e3, ne))
                 if it >= 3:
                     nw = max(v[5], 1)
-                    print("  per warp (kcycles): prologue %.1f wait %.1f slow %.1f loop %.1f flush %.2f"
+                    print("  agg_reduce per warp (kcycles): wait %.1f loads %.1f scan+thr %.1f reduce+atomics %.1f (unused %.2f)"
                           " | max warp %.1f | warps %d tiles %d" % (v[0] / nw / 1e3, v[1] / nw / 1e3,
                           v[2] / nw / 1e3, v[3] / nw / 1e3, v[4] / nw / 1e3, v[6] / 1e3, nw, v[7] // 8))
             if it >= 3:
