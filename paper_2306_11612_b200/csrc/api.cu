@@ -84,7 +84,7 @@ struct dvl_ctx {
   uint32_t* d_err = nullptr;
   float* h_stage = nullptr;          // pinned + mapped: two TF buffers (kMaxN x 4 floats each)
   float* d_hstage = nullptr;         // its device alias (read by the prologue kernel)
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // prologue done with staging buffer i
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // staging buffer i is free once this completes
   int stage_par = 0;
   uint16_t* d_t1 = nullptr;
   uint16_t* d_t2 = nullptr;
@@ -297,12 +297,16 @@ void upload_domains(dvl_ctx* ctx) {
 
 // Put one N x 4 TF into the pinned, mapped staging buffer (after the previous reader of the
 // buffer has finished); the prologue kernel reads it over PCIe.
-// Two buffers alternate, so the host waits for the prologue before the previous one (not the
-// previous one itself) and can enqueue an edit while the GPU still runs the last.
+// Two buffers alternate.  The event of buffer b is recorded when the edit before the one that
+// will use b is staged (before its prologue is enqueued), so it completes once the prologue of
+// the edit before that -- b's last reader -- has run: the host can enqueue an edit while the
+// GPU still runs the last, and no event sits between two kernels of one edit (an event
+// between a kernel and its programmatic dependent would serialise them).
 void stage_tf(dvl_ctx* ctx, const float* rgba, int N) {
   ctx->stage_par ^= 1;
   CK(cudaEventSynchronize(ctx->stage_ev[ctx->stage_par]));
   memcpy(ctx->h_stage + (size_t)ctx->stage_par * 4 * kMaxN, rgba, sizeof(float) * 4 * N);
+  CK(cudaEventRecord(ctx->stage_ev[ctx->stage_par ^ 1], ctx->stream));
 }
 
 // The fused prologue: optional TF install of `member`, pass-1 state reset, max(V_h).
@@ -311,7 +315,6 @@ void launch_prologue(dvl_ctx* ctx, int member, int mode, unsigned long long* zer
   launch_tf_prologue(ctx->d_hstage + (size_t)ctx->stage_par * 4 * kMaxN, member, mode, d.M, ctx->N, d.d_rgba, d.d_tab, d.d_vmin,
                      d.d_vmax, d.d_lo, d.d_inv, ctx->d_maxv, zero, zero_words, ctx->stream);
   CKLAUNCH();
-  if (member >= 0) CK(cudaEventRecord(ctx->stage_ev[ctx->stage_par], ctx->stream));
 }
 
 // Work split of the TMA path for the current TF size: tile size from M, stage ring depth
@@ -986,19 +989,12 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr, ctx->stream);
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
-    if (d.tma) {   // the warp tiles that straddle pixels
-      tic(ctx, PH_BOUND);
-      launch_bin_boundary(p, ctx->d_qtot, W, a, ctx->cell_offset, d.blist, d.bctr, ctx->num_sms,
-                          ctx->stream);
-      CKLAUNCH();
-      toc(ctx, PH_BOUND);
-    }
     dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
     tic(ctx, PH_EPI);
     launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
@@ -1129,19 +1125,12 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr, ctx->stream);
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
-    if (d.tma) {
-      tic(ctx, PH_BOUND);
-      launch_bin_boundary(p, ctx->d_qtot_glob, W, a, ctx->cell_offset, d.blist, d.bctr,
-                          ctx->num_sms, ctx->stream);
-      CKLAUNCH();
-      toc(ctx, PH_BOUND);
-    }
     launch_acc_export(a, W, d.M, (long long*)export_dev, ctx->stream);
     CKLAUNCH();
   } catch (Fail& f) {
@@ -1357,4 +1346,7 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
 // timing experiments: pass-2 phase clock sums (see update_tma.cu); not part of dvl.h
 extern "C" __attribute__((visibility("default"))) int dvl_debug_stats(unsigned long long* out) {
   return dvl::debug_stats(out, true) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int dvl_debug_tl2(unsigned long long* out) {
+  return dvl::debug_tl2(out) == cudaSuccess ? 0 : 1;
 }

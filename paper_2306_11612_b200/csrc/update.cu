@@ -109,6 +109,32 @@ void launch_maxv_approx(int mode, int M, int N, const float2* tab, const float* 
 // straight from the caller-filled pinned staging buffer (mapped host memory: the 16 N
 // bytes cross PCIe inside this kernel, no separate copy), zero the pass-1 look-back state,
 // then (mode 0/1) max(V_h) as maxv_approx_kernel.
+#ifdef DVL_PROF
+// timeline of the prologue and epilogue (globaltimer ns, read by dvl_debug_tl2): slots
+// 2k = ~(first start), 2k+1 = last end; k = 0 prologue, 1 epilogue, 2 epilogue after wait
+__device__ unsigned long long g_tl2[8 + 1 + 64 * 4];   // + step counter, per step (64 ring):
+// prologue start, prologue end, epilogue after wait (block 0), epilogue end
+__device__ __forceinline__ unsigned long long gtime2() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL2_START(k) \
+  if (threadIdx.x == 0) atomicMax(&g_tl2[2 * (k)], ~gtime2());
+#define TL2_END(k) \
+  if (threadIdx.x == 0) atomicMax(&g_tl2[2 * (k) + 1], gtime2());
+cudaError_t debug_tl2(unsigned long long* out) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_tl2, sizeof(g_tl2));
+  static unsigned long long z[8 + 1 + 64 * 4];
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_tl2, z, sizeof(z));
+  return e;
+}
+#else
+#define TL2_START(k)
+#define TL2_END(k)
+cudaError_t debug_tl2(unsigned long long*) { return cudaErrorNotSupported; }
+#endif
+
 __global__ void __launch_bounds__(1024)
 tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M, int N,
                    float4* __restrict__ rgba_all, float2* __restrict__ tab_all,
@@ -118,6 +144,17 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
   // let pass 1 be scheduled now: its producer streams the scalars meanwhile, its consumers
   // wait for this kernel (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  TL2_START(0)
+#ifdef DVL_PROF
+  unsigned step = 0;
+  if (threadIdx.x == 0) {
+    step = (unsigned)atomicAdd(&g_tl2[8], 1ull) & 63u;
+    g_tl2[9 + 4 * step] = gtime2();
+  }
+#define TL2_STEP_END if (threadIdx.x == 0) g_tl2[9 + 4 * step + 1] = gtime2();
+#else
+#define TL2_STEP_END
+#endif
   const int tid = threadIdx.x;
   if (member >= 0) {
     float4* rgba = rgba_all + (int64_t)member * N;
@@ -132,7 +169,11 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
     }
   }
   for (int k = tid; k < zero_words; k += blockDim.x) zero[k] = 0ull;
-  if (mode < 0) return;
+  if (mode < 0) {
+    TL2_END(0)
+    TL2_STEP_END
+    return;
+  }
   __syncthreads();   // the new table is visible to the whole block
   __shared__ int s_i, s_j;
   __shared__ uint32_t s_hi, s_lo;
@@ -184,6 +225,8 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
   if (tid == 0)
     *maxv = mode == 0 ? __fsub_rn(__uint_as_float(s_hi), __uint_as_float(s_lo))
                       : __uint_as_float(s_hi);
+  TL2_END(0)
+  TL2_STEP_END
 }
 
 void launch_tf_prologue(const float* stage, int member, int mode, int M, int N, float4* rgba_all,
@@ -599,7 +642,13 @@ __global__ void __launch_bounds__(256)
 epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
                 dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
                 unsigned long long* bin_hi) {
+  TL2_START(1)
   asm volatile("griddepcontrol.wait;" ::: "memory");   // launched dependent on pass 2
+  TL2_START(2)
+#ifdef DVL_PROF
+  const unsigned step = (unsigned)(*(volatile unsigned long long*)&g_tl2[8] - 1) & 63u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tl2[9 + 4 * step + 2] = gtime2();
+#endif
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (int64_t)M * W) return;
   const int m = (int)(k / W);
@@ -620,6 +669,10 @@ epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rg
   acc.slo[k] = 0ull;
   acc.shi[k] = 0ull;
   out[k] = make_vertex(cnt, mn, mx, sh, sl, rgba + (int64_t)m * N, N);
+  TL2_END(1)
+#ifdef DVL_PROF
+  if (threadIdx.x == 0) atomicMax(&g_tl2[9 + 4 * step + 3], gtime2());
+#endif
 }
 
 __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
