@@ -114,9 +114,12 @@ typedef struct {
 typedef struct {
     float ingest_ms, encode_ms, sort_ms, gather_ms;      /* build phases */
     float maxv_ms, weights_scan_ms;                      /* dvl_update_tf */
-    float bin_reduce_ms, epilogue_ms;                    /* dvl_get_polylines: pass 2 (the
-                                                            streaming part), epilogue */
-    float bin_boundary_ms;                               /* pass 2's boundary warp tiles */
+    float bin_reduce_ms, epilogue_ms;                    /* dvl_get_polylines: pass 2
+                                                            (with its boundary warp tiles),
+                                                            epilogue */
+    float bin_boundary_ms;                               /* 0: kept for the layout (the
+                                                            boundary warp tiles are part of
+                                                            pass 2) */
     int32_t sort_passes;
     int32_t launches;     /* kernels launched since the previous dvl_get_timings call */
 } dvl_timings;

@@ -51,8 +51,6 @@ struct Dataset {
   unsigned long long* meta2 = nullptr;          // n_pad / 128: the warp's running q sum in its
                                                 // pass-1 chunk before the warp tile's tile
   void* agg = nullptr;                          // D3: per warp tile and member t statistics
-  unsigned long long* blist = nullptr;          // 2 x n_pad / 128: pass-2 boundary warp tiles
-  uint32_t* bctr = nullptr;                     // their count + done counter (self-resetting)
 };
 
 }  // namespace
@@ -194,7 +192,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
-                d.tile_meta, d.blist, d.bctr, d.meta2, d.agg};
+                d.tile_meta, d.meta2, d.agg};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -406,9 +404,8 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
                               ctx->d_qtot, d.tile_meta, d.meta2, ctx->stream);
     CKLAUNCH();
     if (export_q) {
-      launch_bin_reduce_tma(false, true, p, d.plan, d.grid, d.chunk_prefix,
-                            ctx->d_qtot, 2, Acc{}, 0, ctx->d_err, q_out, d.tile_meta, d.blist, d.bctr, ctx->num_sms,
-                            ctx->stream);
+      launch_q_export_tma(false, p, d.plan, d.grid, d.chunk_prefix, ctx->d_qtot, ctx->d_err, q_out,
+                          d.tile_meta, ctx->stream);
       CKLAUNCH();
     }
   } else {
@@ -804,9 +801,6 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
       d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
       d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
       d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
-      d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
-      d.bctr = dalloc<uint32_t>(ctx, 2);
-      CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), ctx->stream));
     }
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));

@@ -105,15 +105,10 @@ void launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned l
                        const unsigned long long* qtot, uint32_t W, const Acc& acc,
                        uint64_t cell_offset, uint32_t* err, const unsigned long long* meta,
                        const unsigned long long* meta2, const void* agg, cudaStream_t st);
-void launch_bin_reduce_tma(bool smem_tab, bool export_q, const UpdParams& p, const TmaPlan& plan,
-                           int grid, const unsigned long long* chunk_prefix,
-                           const unsigned long long* qtot, uint32_t W, const Acc& acc,
-                           uint64_t cell_offset, uint32_t* err, unsigned long long* q_out,
-                           const unsigned long long* meta, unsigned long long* blist,
-                           uint32_t* bctr, int num_sms, cudaStream_t st);
-void launch_bin_boundary(const UpdParams& p, const unsigned long long* qtot, uint32_t W,
-                         const Acc& acc, uint64_t cell_offset, const unsigned long long* blist,
-                         uint32_t* bctr, int num_sms, cudaStream_t st);
+void launch_q_export_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,
+                         const unsigned long long* chunk_prefix, const unsigned long long* qtot,
+                         uint32_t* err, unsigned long long* q_out, const unsigned long long* meta,
+                         cudaStream_t st);
 size_t bin_reduce_smem(int items, int M, int N, bool smem_tab);
 
 }  // namespace dvl
