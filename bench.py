@@ -423,20 +423,26 @@ def run_native(args, rank, world, local):
     # ---- roofline of the dominant kernel (algorithmic bytes, design D3)
     peak, peak_src = load_peaks()
     per_kernel = {k: v / args.steps for k, v in kern.items()}
-    # pass 1 streams every member scalar and level; pass 2 (design D3) streams, per warp tile
-    # of 128 cells, its q sum and running sum (16 B) and its M t-statistics (16 M B)
-    bytes_cell = {"weights_scan_ms": 4 * M + 1, "bin_reduce_ms": (16 * M + 16) / 128}
+    # pass 1 streams every member scalar and level -- with the edit cache (M >= 3, the
+    # repeated edits of one member timed here) the edited member's scalar, the cached alpha
+    # range of the others (8 B) and the level; pass 2 (design D3) streams, per warp tile of
+    # 128 cells, its q sum and running sum (16 B) and its M t-statistics (16 M B)
+    tma = M <= 16
+    edit_cache = tma and M >= 3 and os.environ.get("DVL_EDIT_CACHE", "1") != "0"
+    bytes_cell = {"weights_scan_ms": 13 if edit_cache else 4 * M + 1,
+                  "bin_reduce_ms": (16 * M + 16) / 128}
     dom = max(bytes_cell, key=lambda k: per_kernel[k])
     alg_bytes = int(n * bytes_cell[dom])
     achieved = alg_bytes / (per_kernel[dom] / 1e3) / 1e9
-    tma = M <= 16
     kname = {"weights_scan_ms": "weights_reduce_tma" if tma else "weights_scan_kernel",
              "bin_reduce_ms": "agg_reduce" if tma else "bin_reduce_kernel"}[dom]
     traffic = load_traffic(kname)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "bytes_per_cell": bytes_cell[dom]}
+            "bytes_per_cell": bytes_cell[dom],
+            "pass1_reads": ("edited member scalar + cached alpha range of the others + level"
+                            if edit_cache else "every member scalar + level")}
     pass_bytes = n * (bytes_cell["weights_scan_ms"] + bytes_cell["bin_reduce_ms"])
     update_kernels_ms = per_kernel["weights_scan_ms"] + per_kernel["bin_reduce_ms"]
     cpu = None

@@ -51,6 +51,11 @@ struct Dataset {
   unsigned long long* meta2 = nullptr;          // n_pad / 128: the warp's running q sum in its
                                                 // pass-1 chunk before the warp tile's tile
   void* agg = nullptr;                          // D3: per warp tile and member t statistics
+  // edit cache (TMA path, M >= 3): per cell the min / max of the alpha bits of the members
+  // other than cache_member, valid while their TFs and the domains stay as they were
+  uint32_t* cmin = nullptr;
+  uint32_t* cmax = nullptr;
+  int cache_member = -1;
 };
 
 }  // namespace
@@ -103,6 +108,7 @@ struct dvl_ctx {
   int launches = 0;
   int num_sms = 148;
   int acc_par = 0;                        // which lo / hi copy the next call uses
+  bool edit_cache = true;                 // DVL_EDIT_CACHE=0: every edit reads every member
   int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
   int stages_override = 0;
@@ -192,7 +198,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
-                d.tile_meta, d.meta2, d.agg};
+                d.tile_meta, d.meta2, d.agg, d.cmin, d.cmax};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -266,6 +272,9 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.l2_keep = ctx->l2_keep;
   p.prod_sleep = ctx->prod_sleep;
   p.dbg = ctx->dbg;
+  p.cmin = d.cmin;
+  p.cmax = d.cmax;
+  p.cmember = -1;
   return p;
 }
 
@@ -281,6 +290,7 @@ int compute_shift(dvl_ctx* ctx) {
 
 void upload_domains(dvl_ctx* ctx) {
   const int M = ctx->ds.M;
+  ctx->ds.cache_member = -1;   // the alphas depend on the domains
   CK(cudaMemcpyAsync(ctx->ds.d_lo, ctx->lo_h.data(), sizeof(float) * M, cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaMemcpyAsync(ctx->ds.d_inv, ctx->inv_h.data(), sizeof(float) * M,
@@ -397,11 +407,36 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
     CKLAUNCH();
   }
   toc(ctx, PH_MAXV);
+  // the edit cache: an edit of member e reads only e's scalars and the cached alpha range
+  // of the others when the cache holds them (kCache), else pass 1 reads every member and
+  // (re)writes the cache for e (kWrite).  Any other TF or domain change invalidates it.
+  int cmode = 0;
+  if (member >= 0) {
+    if (d.tma && d.M >= 3 && ctx->edit_cache && !export_q) {
+      if (!d.cmin) {
+        try {
+          d.cmin = dalloc<uint32_t>(ctx, (size_t)d.n_pad);
+          d.cmax = dalloc<uint32_t>(ctx, (size_t)d.n_pad);
+        } catch (Fail&) {   // no room for it: every edit reads every member
+          dfree(ctx, d.cmin);
+          d.cmin = nullptr;
+          ctx->edit_cache = false;
+        }
+      }
+      if (d.cmin) {
+        cmode = d.cache_member == member ? 1 : 2;
+        p.cmin = d.cmin;
+        p.cmax = d.cmax;
+        p.cmember = member;
+      }
+    }
+    d.cache_member = cmode ? member : -1;
+  }
   tic(ctx, PH_WSCAN);
   if (d.tma) {
     launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid1, d.chunk_status,
                               reinterpret_cast<uint32_t*>(d.chunk_status + d.grid1), d.chunk_prefix,
-                              ctx->d_qtot, d.tile_meta, d.meta2, ctx->stream);
+                              ctx->d_qtot, d.tile_meta, d.meta2, cmode, ctx->stream);
     CKLAUNCH();
     if (export_q) {
       launch_q_export_tma(false, p, d.plan, d.grid, d.chunk_prefix, ctx->d_qtot, ctx->d_err, q_out,
@@ -480,6 +515,7 @@ void identity_tf_host(std::vector<float>& tf, int N) {
 }
 
 void set_all_tfs(dvl_ctx* ctx, const std::vector<float>& tf, int N) {
+  ctx->ds.cache_member = -1;   // every member's TF changes
   for (int m = 0; m < ctx->ds.M; ++m) {
     stage_tf(ctx, tf.data(), N);
     launch_prologue(ctx, m, -1, nullptr, 0);
@@ -572,6 +608,7 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
     if (const char* e = getenv("DVL_STAGES2")) ctx->stages_override = atoi(e);
     if (const char* e = getenv("DVL_DBG")) ctx->dbg = atoi(e);
+    if (const char* e = getenv("DVL_EDIT_CACHE")) ctx->edit_cache = atoi(e) != 0;
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);

@@ -68,6 +68,11 @@ struct UpdParams {
   int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
   uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
   int dbg;                 // timing experiments only: 1 skip pass-2 folds, 2 skip pass-1 weights
+  // edit cache (repeated TF edits of one member): per cell the min / max of the alpha bits
+  // of the members other than cmember (identity 0xffffffff / 0 when there are none)
+  uint32_t* cmin;
+  uint32_t* cmax;
+  int cmember;
 };
 
 // Work split of the TMA-pipelined update kernels (host-computed).

@@ -93,10 +93,11 @@ int tma_blocks_per_sm(int M, bool smem_tab, const TmaPlan& plan, int pass);
 int tma_tile2_cells(int M);
 int tma_pass2_ctas_per_sm(int M);
 int tma_warp_tile_cells();
+// cmode: 0 every member, 1 edited member + edit cache, 2 every member + write the cache
 void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,
                                unsigned long long* chunk_status, uint32_t* ctr,
                                unsigned long long* chunk_prefix, unsigned long long* qtot,
-                               unsigned long long* meta, unsigned long long* meta2,
+                               unsigned long long* meta, unsigned long long* meta2, int cmode,
                                cudaStream_t st);
 size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);   // DVL_PROF builds

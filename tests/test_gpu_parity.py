@@ -241,6 +241,61 @@ def test_repeated_edits_and_determinism(dvl):
     ctx.close()
 
 
+@pytest.mark.parametrize("M", [3, 4, 5, 8, 16])
+def test_edit_cache_sequences(dvl, M):
+    """The edit cache (repeated edits of one member read that member and the cached alpha
+    range of the others): edit sequences that switch members, change a domain, reset the
+    TFs and change P / eps in between, each checked against the oracle, and against a
+    context with the cache disabled (bit for bit)."""
+    import os
+    lower, level = octree(32, 3, 60 + M)
+    scal = scalars(len(level), M, 61 + M, nan_frac=0.01)
+    B = o.build(lower, level, scal)
+    ctx = make_ctx(dvl)
+    ctx.build(lower, level, scal)
+    os.environ["DVL_EDIT_CACHE"] = "0"
+    try:
+        ref_ctx = make_ctx(dvl)
+    finally:
+        del os.environ["DVL_EDIT_CACHE"]
+    ref_ctx.build(lower, level, scal)
+    tfs = tfs_for(M, 256, 62)
+    for c in (ctx, ref_ctx):
+        for m in range(M):
+            c.update_tf(m, tfs[m])
+    domain = [[float(np.nanmin(scal[m])), float(np.nanmax(scal[m]))] for m in range(M)]
+    W = 700
+    steps = [("edit", 0), ("edit", 0), ("edit", 0), ("edit", M - 1), ("edit", M - 1), ("edit", 0),
+             ("domain", 1), ("edit", 0), ("edit", 0), ("params", 2.0), ("edit", 0), ("reset", None),
+             ("edit", 1), ("edit", 1), ("params", 1.0), ("edit", 1)]
+    P = 1.0
+    for k, (op, arg) in enumerate(steps):
+        for c in (ctx, ref_ctx):
+            if op == "edit":
+                tfs[arg] = synth.tf_edit(3, k, 256, member=arg)
+                c.update_tf(arg, tfs[arg])
+            elif op == "domain":
+                lo, hi = domain[arg][0] + 0.25, domain[arg][1] - 0.25
+                c.set_domain(arg, lo, hi)
+            elif op == "params":
+                P = arg
+                c.set_params(P, 0.025, "conservative")
+            elif op == "reset":
+                c.reset_tfs(256)
+        if op == "domain":
+            domain[arg] = [domain[arg][0] + 0.25, domain[arg][1] - 0.25]
+        if op == "reset":
+            tfs = np.stack([o.identity_tf(256)] * M)
+        a = ctx.get_polylines(W)
+        b = ref_ctx.get_polylines(W)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (k, op)
+        U = o.update(B, tfs, W, P=P, domain=np.array(domain, f32))
+        g = dict(out=a, info=ctx.info(), Q=ctx.get_prefix(), ranges=ctx.get_bin_ranges(W))
+        check_update(U, B, tfs, g, W)
+    ctx.close()
+    ref_ctx.close()
+
+
 def test_errors(dvl):
     ctx = make_ctx(dvl)
     with pytest.raises(dvl.DvlError) as e:
