@@ -639,36 +639,61 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
 // (current copy), m = 0 writes the bin ranges and restores the identity of the other copy;
 // every thread restores the identity of its member partials.
 __global__ void __launch_bounds__(256)
-epilogue_kernel(Acc acc, uint32_t W, int M, int N, const float4* __restrict__ rgba,
+epilogue_kernel(Acc acc, WDiv wd, int M, int N, const float4* __restrict__ rgba,
                 dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
-                unsigned long long* bin_hi) {
+                unsigned long long* bin_hi, bool stage_tf) {
+  const uint32_t W = wd.d;   // M W <= 2^20: 32-bit entry indices, divisions by W via WDiv
+  extern __shared__ float4 s_tf[];
   TL2_START(1)
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // launched dependent on pass 2
-  TL2_START(2)
+  // the TF rows of the block's members into shared memory before the wait (pass 2 lets this
+  // kernel start only once pass 1 -- and so the prologue that wrote them -- is complete)
+  const uint32_t k0 = blockIdx.x * blockDim.x;
+  const int m0 = (int)wd.div(k0);
+  if (stage_tf) {
+    const int m1 = min(M - 1, (int)wd.div(k0 + blockDim.x - 1));
+    const int cnt = (m1 - m0 + 1) * N;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_tf[i] = rgba[(int64_t)m0 * N + i];
+    __syncthreads();
+  }
+  const uint32_t k = k0 + threadIdx.x;
+  const int m = min((int)wd.div(k), M - 1);
+  const uint32_t x = k - (uint32_t)m * W;
+  const float4* tf = stage_tf ? s_tf + (m - m0) * N : rgba + (int64_t)m * N;
+  // The vertex code runs twice: first on a dummy entry before the wait, so that its
+  // instructions are in the SM's instruction cache when the real entry comes (this kernel
+  // is short and runs once per edit: cold instruction fetches were most of its time).
+  dvl_vertex vtx;
+  uint32_t cnt = 1, mn = 0, mx = 0;
+  unsigned long long sl = 0, sh = 0;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // launched dependent on pass 2
+      TL2_START(2)
+      TL2_END(2)
+      if (k >= (uint32_t)M * W) return;
+      const unsigned long long lo = acc.lo[x], hi = acc.hi[x];
+      if (m == 0) {
+        bin_lo[x] = lo;
+        bin_hi[x] = hi;
+        acc.lo2[x] = ~0ull;
+        acc.hi2[x] = 0ull;
+      }
+      cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
+      mn = acc.tmin[k];
+      mx = acc.tmax[k];
+      sum_words(acc.slo[k], acc.shi[k], sh, sl);
+      acc.tmin[k] = 0xffffffffu;
+      acc.tmax[k] = 0u;
+      acc.slo[k] = 0ull;
+      acc.shi[k] = 0ull;
+    }
+    vtx = make_vertex(cnt, mn, mx, sh, sl, tf, N);
+  }
 #ifdef DVL_PROF
   const unsigned step = (unsigned)(*(volatile unsigned long long*)&g_tl2[8] - 1) & 63u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_tl2[9 + 4 * step + 2] = gtime2();
 #endif
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= (int64_t)M * W) return;
-  const int m = (int)(k / W);
-  const uint32_t x = (uint32_t)(k - (int64_t)m * W);
-  const unsigned long long lo = acc.lo[x], hi = acc.hi[x];
-  if (m == 0) {
-    bin_lo[x] = lo;
-    bin_hi[x] = hi;
-    acc.lo2[x] = ~0ull;
-    acc.hi2[x] = 0ull;
-  }
-  const uint32_t cnt = lo <= hi ? (uint32_t)(hi - lo + 1) : 0u;
-  const uint32_t mn = acc.tmin[k], mx = acc.tmax[k];
-  unsigned long long sl, sh;
-  sum_words(acc.slo[k], acc.shi[k], sh, sl);
-  acc.tmin[k] = 0xffffffffu;
-  acc.tmax[k] = 0u;
-  acc.slo[k] = 0ull;
-  acc.shi[k] = 0ull;
-  out[k] = make_vertex(cnt, mn, mx, sh, sl, rgba + (int64_t)m * N, N);
+  out[k] = vtx;
   TL2_END(1)
 #ifdef DVL_PROF
   if (threadIdx.x == 0) atomicMax(&g_tl2[9 + 4 * step + 3], gtime2());
@@ -695,16 +720,22 @@ void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgb
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                      cudaStream_t st) {
   const int grid = (int)(((int64_t)M * W + 255) / 256);
+  // members a block of 256 entries spans, and their TF rows in shared memory if they fit
+  const int64_t rows = std::min<int64_t>(M, (255 + W - 1) / W + 1);
+  const size_t tf_bytes = (size_t)rows * N * sizeof(float4);
+  const bool stage_tf = tf_bytes <= 32 * 1024;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = stage_tf ? tf_bytes : 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  (void)cudaLaunchKernelEx(&cfg, epilogue_kernel, acc, W, M, N, rgba, out, bin_lo, bin_hi);
+  (void)cudaLaunchKernelEx(&cfg, epilogue_kernel, acc, WDiv::make(W), M, N, rgba, out, bin_lo, bin_hi,
+                           stage_tf);
 }
 
 void launch_acc_init(const Acc& acc, uint32_t W, int M, cudaStream_t st) {

@@ -20,7 +20,8 @@ BASE = SLOTS - 32
 NAMES = [("pass1 entry", 0), ("pass1 after wait", 10), ("pass1 stream end", 11), ("pass1 end", 1),
          ("agg entry", 2), ("agg after wait", 4), ("agg end", 3)]
 NAMES2 = [("prologue start", 0), ("prologue end", 1), ("epilogue entry", 2),
-          ("epilogue after wait", 4), ("epilogue end", 3)]
+          ("epilogue after wait", 4), ("epilogue after wait (last)", 5),
+          ("epilogue loads done (last)", 7), ("epilogue vertex done (last)", 6), ("epilogue end", 3)]
 ALL = NAMES2[:2] + NAMES + NAMES2[2:]
 
 
@@ -62,8 +63,10 @@ def main():
         return
     rows = []
     st = torch.cuda.ExternalStream(ctx.stream)
+    do_flush = os.environ.get("TL_FLUSH", "1") == "1"
     for it in range(24):
-        flush.zero_()
+        if do_flush:
+            flush.zero_()
         torch.cuda.synchronize()
         lib.dvl_debug_stats(buf)
         lib.dvl_debug_tl2(buf2)
@@ -87,7 +90,7 @@ def main():
             t[nm] = int(x)
         for nm, k in NAMES2:
             x = int(v2[k])
-            if k % 2 == 0:
+            if k % 2 == 0 and k != 6:   # (slot 6: a plain max stamp)
                 x = (~np.uint64(x)) & np.uint64(0xFFFFFFFFFFFFFFFF) if x else 0
             t[nm] = int(x)
         t0 = t["pass1 entry"]
