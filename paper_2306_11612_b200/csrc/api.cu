@@ -1378,6 +1378,9 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
 extern "C" __attribute__((visibility("default"))) int dvl_debug_stats(unsigned long long* out) {
   return dvl::debug_stats(out, true) == cudaSuccess ? 0 : 1;
 }
+extern "C" __attribute__((visibility("default"))) int dvl_debug_bt(unsigned long long* out) {
+  return dvl::debug_bt(out) == cudaSuccess ? 0 : 1;
+}
 extern "C" __attribute__((visibility("default"))) int dvl_debug_tl2(unsigned long long* out) {
   return dvl::debug_tl2(out) == cudaSuccess ? 0 : 1;
 }

@@ -100,7 +100,8 @@ void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan&
                                unsigned long long* meta, unsigned long long* meta2, int cmode,
                                cudaStream_t st);
 size_t agg_bytes(int M, int64_t nwt);
-cudaError_t debug_tl2(unsigned long long* out);   // DVL_PROF builds
+cudaError_t debug_tl2(unsigned long long* out);
+cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds
 void launch_agg_build(const UpdParams& p, void* agg, int64_t nwt, int num_sms, cudaStream_t st);
 void launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned long long* chunk_prefix,
                        const unsigned long long* qtot, uint32_t W, const Acc& acc,
