@@ -37,6 +37,13 @@ def main():
         lib.dvl_debug_bt(bt)
         ctx.update_tf(0, synth.tf_edit(1, 1 + it, 256, member=0))
         ctx.get_polylines(W, out=out)
+        if os.environ.get("AGG_TWICE") == "1":   # the reduction again, its code now warm
+            torch.cuda.synchronize()
+            lib.dvl_debug_stats(buf)
+            lib.dvl_debug_bt(bt)
+            if os.environ.get("AGG_FLUSH") == "1":
+                flush.zero_()
+            ctx.get_polylines(W, out=out)
         torch.cuda.synchronize()
         lib.dvl_debug_stats(buf)
         lib.dvl_debug_bt(bt)
