@@ -2,8 +2,10 @@
 
 Prints, per kernel (short name), the launch count and mean / total device time, and the
 share of each dvl::* update kernel in the TF-update step (maxv/prologue, pass 1, pass 2,
-epilogue).  ncu serialises launches and runs them cold-cache, so compare shares with the
-live CUDA-event numbers of bench.py, not absolute times.
+epilogue), from the mean of each update kernel's last STEADY launches: the steady state of
+bench.py's repeated edits of one member (the first edits of each member build the edit cache
+and run longer).  ncu serialises launches and runs them cold-cache, so compare shares with
+the live CUDA-event numbers of bench.py, not absolute times.
 
 usage: python profiles/summarize_launches.py gpurun_out/launches_r01.csv > profiles/r01_launches.md
 """
@@ -13,6 +15,7 @@ import re
 import sys
 
 # the kernels of one TF-update step (acc_init runs once per context / pixel count)
+STEADY = 8
 UPDATE = ("tf_prologue_kernel", "maxv_exact_kernel", "weights_reduce_tma", "agg_reduce",
           "bin_boundary", "epilogue_kernel", "weights_scan_kernel", "bin_reduce_kernel")
 
@@ -44,13 +47,17 @@ def main(path):
     print("|---|---|---|---|---|---|")
     for name, (c, tot, g, b) in agg.items():
         print(f"| {name} | {g} | {b} | {c} | {tot / c / 1e3:.2f} | {tot / 1e3:.1f} |")
-    upd = {k: v for k, v in agg.items() if k in UPDATE}
-    step = sum(v[1] / v[0] for v in upd.values())
-    print("\n## TF-update step (mean launch of each update kernel)\n")
+    per = collections.OrderedDict()
+    for name, ns, _, _ in launches:
+        if name in UPDATE:
+            per.setdefault(name, []).append(ns)
+    upd = {k: sum(v[-STEADY:]) / len(v[-STEADY:]) for k, v in per.items()}
+    step = sum(upd.values())
+    print(f"\n## TF-update step (mean of the last {STEADY} launches of each update kernel)\n")
     print("| kernel | mean us | share of step |")
     print("|---|---|---|")
-    for name, (c, tot, _, _) in upd.items():
-        print(f"| {name} | {tot / c / 1e3:.2f} | {tot / c / step:.3f} |")
+    for name, ns in upd.items():
+        print(f"| {name} | {ns / 1e3:.2f} | {ns / step:.3f} |")
     print(f"| **sum** | {step / 1e3:.2f} | 1.000 |")
 
 
