@@ -135,6 +135,8 @@ cudaError_t debug_tl2(unsigned long long* out) {
 cudaError_t debug_tl2(unsigned long long*) { return cudaErrorNotSupported; }
 #endif
 
+constexpr int kProloguAlpha = 12 * 1024;   // alphas the prologue stages in shared memory (48 KB)
+
 __global__ void __launch_bounds__(1024)
 tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M, int N,
                    float4* __restrict__ rgba_all, float2* __restrict__ tab_all,
@@ -156,25 +158,10 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
 #define TL2_STEP_END
 #endif
   const int tid = threadIdx.x;
-  if (member >= 0) {
-    float4* rgba = rgba_all + (int64_t)member * N;
-    float2* tab = tab_all + (int64_t)member * N;
-    for (int i = tid; i < N; i += blockDim.x) {
-      float4 e = make_float4(__fadd_rn(stage[4 * i], 0.0f), __fadd_rn(stage[4 * i + 1], 0.0f),
-                             __fadd_rn(stage[4 * i + 2], 0.0f), __fadd_rn(stage[4 * i + 3], 0.0f));
-      rgba[i] = e;
-      float d = 0.0f;
-      if (i + 1 < N) d = __fsub_rn(__fadd_rn(stage[4 * i + 7], 0.0f), e.w);
-      tab[i] = make_float2(e.w, d);
-    }
-  }
-  for (int k = tid; k < zero_words; k += blockDim.x) zero[k] = 0ull;
-  if (mode < 0) {
-    TL2_END(0)
-    TL2_STEP_END
-    return;
-  }
-  __syncthreads();   // the new table is visible to the whole block
+  // Every input is requested up front, so that the PCIe read of the staged TF, the domain
+  // loads and (maxV from shared memory, s_alpha) the other members' alpha columns overlap.
+  extern __shared__ float s_alpha[];   // M x N alphas when s_alpha_ok (the launch sized it)
+  const bool s_alpha_ok = mode >= 0 && M * N <= kProloguAlpha;
   __shared__ int s_i, s_j;
   __shared__ uint32_t s_hi, s_lo;
   if (tid == 0) {
@@ -183,11 +170,37 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
     s_hi = 0;
     s_lo = 0xffffffffu;
   }
-  __syncthreads();
+  if (s_alpha_ok)
+    for (int k = tid; k < M * N; k += blockDim.x)
+      if (k / N != member) s_alpha[k] = tab_all[k].x;
+  float tl = 0.0f, th = 0.0f;
+  if (mode >= 0 && tid < M) {
+    tl = norm_t(vmin[tid], lo[tid], inv[tid]);
+    th = norm_t(vmax[tid], lo[tid], inv[tid]);
+  }
+  if (member >= 0) {
+    float4* rgba = rgba_all + (int64_t)member * N;
+    float2* tab = tab_all + (int64_t)member * N;
+    for (int i = tid; i < N; i += blockDim.x) {
+      const float4 r = reinterpret_cast<const float4*>(stage)[i];   // one 16-byte PCIe read
+      const float4 e = make_float4(__fadd_rn(r.x, 0.0f), __fadd_rn(r.y, 0.0f),
+                                   __fadd_rn(r.z, 0.0f), __fadd_rn(r.w, 0.0f));
+      rgba[i] = e;
+      float d = 0.0f;
+      if (i + 1 < N) d = __fsub_rn(__fadd_rn(stage[4 * i + 7], 0.0f), e.w);
+      tab[i] = make_float2(e.w, d);
+      if (s_alpha_ok) s_alpha[member * N + i] = e.w;
+    }
+  }
+  for (int k = tid; k < zero_words; k += blockDim.x) zero[k] = 0ull;
+  if (mode < 0) {
+    TL2_END(0)
+    TL2_STEP_END
+    return;
+  }
+  __syncthreads();   // the new table and the alphas are visible to the whole block
   const float nm1 = (float)(N - 1);
-  for (int m = tid; m < M; m += blockDim.x) {
-    float tl = norm_t(vmin[m], lo[m], inv[m]);
-    float th = norm_t(vmax[m], lo[m], inv[m]);
+  if (tid < M) {
     int i = (int)floorf(__fmul_rn(tl, nm1));
     int j = (int)ceilf(__fmul_rn(th, nm1));
     j = min(j, N - 1);
@@ -196,19 +209,20 @@ tf_prologue_kernel(const float* __restrict__ stage, int member, int mode, int M,
   }
   __syncthreads();
   const int i = s_i, j = s_j, w = j - i + 1;
+  auto alpha = [&](int m, int a) { return s_alpha_ok ? s_alpha[m * N + a] : tab_all[m * N + a].x; };
   uint32_t hi = 0, lo_ = 0xffffffffu;
   if (mode == 0) {
     for (int k = tid; k < M * w; k += blockDim.x) {
       int m = k / w, a = i + k % w;
-      uint32_t b = __float_as_uint(tab_all[m * N + a].x);   // alpha >= +0: bits order as values
+      uint32_t b = __float_as_uint(alpha(m, a));   // alpha >= +0: bits order as values
       hi = max(hi, b);
       lo_ = min(lo_, b);
     }
   } else {
     for (int a = i + tid; a <= j; a += blockDim.x) {
-      float mx = tab_all[a].x, mn = mx;
+      float mx = alpha(0, a), mn = mx;
       for (int m = 1; m < M; ++m) {
-        float v = tab_all[m * N + a].x;
+        float v = alpha(m, a);
         mx = v > mx ? v : mx;
         mn = v < mn ? v : mn;
       }
@@ -233,8 +247,9 @@ void launch_tf_prologue(const float* stage, int member, int mode, int M, int N, 
                         float2* tab_all, const float* vmin, const float* vmax, const float* lo,
                         const float* inv, float* maxv, unsigned long long* zero, int zero_words,
                         cudaStream_t st) {
-  tf_prologue_kernel<<<1, 1024, 0, st>>>(stage, member, mode, M, N, rgba_all, tab_all, vmin, vmax,
-                                         lo, inv, maxv, zero, zero_words);
+  const size_t sm = mode >= 0 && M * N <= kProloguAlpha ? sizeof(float) * (size_t)M * N : 0;
+  tf_prologue_kernel<<<1, 1024, sm, st>>>(stage, member, mode, M, N, rgba_all, tab_all, vmin, vmax,
+                                          lo, inv, maxv, zero, zero_words);
 }
 
 // ------------------------------------------------------------ per-cell weights (U1)
