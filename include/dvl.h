@@ -184,7 +184,9 @@ dvl_status dvl_reset_tfs(dvl_ctx *ctx, uint32_t N);
  *   W    2 <= W <= 65536
  *   out  M x W dvl_vertex, member-major (out[m * W + x]), in memory space `where`
  * Uses the weights of the last update (the identity TFs after a build).  Host output
- * synchronises.  Errors: STATE, INVAL, DEGENERATE (all weights are 0), CUDA. */
+ * synchronises; page-locked host output (16-byte aligned) is written by the last kernel
+ * directly (zero copy), pageable host output through one device-to-host copy.  Errors:
+ * STATE, INVAL, DEGENERATE (all weights are 0), CUDA. */
 dvl_status dvl_get_polylines(dvl_ctx *ctx, uint32_t W, dvl_vertex *out, dvl_mem where);
 
 /* ---- sharding: one context per GPU, each holding a contiguous range of the global curve

@@ -1026,24 +1026,38 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
     CKLAUNCH();
     toc(ctx, PH_BREDUCE);
+    // a page-locked host destination is written by the epilogue itself (zero copy through
+    // its device alias); pageable host memory goes through the context's device buffer
     dvl_vertex* dst = where == DVL_MEM_DEVICE ? out : ctx->d_out;
+    bool direct = false;
+    if (where == DVL_MEM_HOST) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, out) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+          at.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(at.devicePointer) & 15) == 0) {
+        dst = static_cast<dvl_vertex*>(at.devicePointer);
+        direct = true;
+      }
+      (void)cudaGetLastError();
+    }
+    // the error word lands in the context's mapped staging (written by the epilogue)
+    const bool check = where == DVL_MEM_HOST || maybe_degenerate(ctx);
+    uint32_t* herr_p = reinterpret_cast<uint32_t*>(ctx->h_stage + 2 * 4 * kMaxN);
+    uint32_t* herr_dev = reinterpret_cast<uint32_t*>(ctx->d_hstage + 2 * 4 * kMaxN);
     tic(ctx, PH_EPI);
-    launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->stream);
+    launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->d_err,
+                    check ? herr_dev : nullptr, ctx->stream);
     CKLAUNCH();
     ctx->acc_par ^= 1;   // this call's copy is restored by the next call's epilogue
     toc(ctx, PH_EPI);
     ctx->last_W = W;
-    if (where == DVL_MEM_HOST) {
-      // page-locked destination: one async DMA; pageable: the driver's staged copy
+    if (where == DVL_MEM_HOST && !direct) {
+      // pageable destination: the driver's staged copy
       CK(cudaMemcpyAsync(out, ctx->d_out, sizeof(dvl_vertex) * (size_t)W * d.M,
                          cudaMemcpyDeviceToHost, ctx->stream));
     }
-    if (where == DVL_MEM_HOST || maybe_degenerate(ctx)) {
-      // the error word through the context's pinned staging (an async copy, one sync)
-      uint32_t* herr_p = reinterpret_cast<uint32_t*>(ctx->h_stage + 2 * 4 * kMaxN);
-      CK(cudaMemcpyAsync(herr_p, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (check) {
       CK(cudaStreamSynchronize(ctx->stream));
-      const uint32_t herr = *herr_p;
+      const uint32_t herr = *(volatile uint32_t*)herr_p;
       if (herr & kErrDegenerate) {
         CK(cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
         ctx->last_W = 0;

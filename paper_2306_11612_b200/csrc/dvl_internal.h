@@ -77,9 +77,10 @@ void launch_acc_export(const Acc& acc, uint32_t W, int M, long long* out, cudaSt
 void launch_epilogue_merged(const long long* merged, uint32_t W, int M, int N, const float4* rgba,
                             dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
                             cudaStream_t st);
+// err_host (device alias of mapped host memory, or nullptr): receives the error word
 void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
-                     cudaStream_t st);
+                     const uint32_t* err, uint32_t* err_host, cudaStream_t st);
 void launch_acc_init(const Acc& acc, uint32_t W, int M, cudaStream_t st);
 cudaError_t prepare_update_kernels();
 

@@ -656,7 +656,8 @@ bin_reduce_kernel(UpdParams p, const unsigned long long* __restrict__ tile_prefi
 __global__ void __launch_bounds__(256)
 epilogue_kernel(Acc acc, WDiv wd, int M, int N, const float4* __restrict__ rgba,
                 dvl_vertex* __restrict__ out, unsigned long long* bin_lo,
-                unsigned long long* bin_hi, bool stage_tf) {
+                unsigned long long* bin_hi, bool stage_tf, const uint32_t* err,
+                volatile uint32_t* err_host) {
   const uint32_t W = wd.d;   // M W <= 2^20: 32-bit entry indices, divisions by W via WDiv
   extern __shared__ float4 s_tf[];
   TL2_START(1)
@@ -686,6 +687,8 @@ epilogue_kernel(Acc acc, WDiv wd, int M, int N, const float4* __restrict__ rgba,
       asm volatile("griddepcontrol.wait;" ::: "memory");   // launched dependent on pass 2
       TL2_START(2)
       TL2_END(2)
+      // the error word of this edit to the host's mapped staging (no separate copy)
+      if (err_host && k == 0) *err_host = *(volatile const uint32_t*)err;
       if (k >= (uint32_t)M * W) return;
       const unsigned long long lo = acc.lo[x], hi = acc.hi[x];
       if (m == 0) {
@@ -708,7 +711,10 @@ epilogue_kernel(Acc acc, WDiv wd, int M, int N, const float4* __restrict__ rgba,
 #ifdef DVL_PROF
   const unsigned step = (unsigned)(*(volatile unsigned long long*)&g_tl2[8] - 1) & 63u;
 #endif
-  out[k] = vtx;
+  // two 16-byte stores (the output may be mapped host memory: whole lines over PCIe)
+  float4* o = reinterpret_cast<float4*>(out + k);
+  o[0] = make_float4(vtx.t_min, vtx.t_max, vtx.t_mean, vtx.y);
+  o[1] = make_float4(vtx.r, vtx.g, vtx.b, __uint_as_float(vtx.count));
   TL2_END(1)
 #ifdef DVL_PROF
   if (threadIdx.x == 0) atomicMax(&g_tl2[9 + 4 * step + 3], gtime2());
@@ -733,7 +739,7 @@ __global__ void acc_init_kernel(Acc acc, uint32_t W, int M) {
 
 void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgba,
                      dvl_vertex* out, unsigned long long* bin_lo, unsigned long long* bin_hi,
-                     cudaStream_t st) {
+                     const uint32_t* err, uint32_t* err_host, cudaStream_t st) {
   const int grid = (int)(((int64_t)M * W + 255) / 256);
   // members a block of 256 entries spans, and their TF rows in shared memory if they fit
   const int64_t rows = std::min<int64_t>(M, (255 + W - 1) / W + 1);
@@ -750,7 +756,7 @@ void launch_epilogue(const Acc& acc, uint32_t W, int M, int N, const float4* rgb
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   (void)cudaLaunchKernelEx(&cfg, epilogue_kernel, acc, WDiv::make(W), M, N, rgba, out, bin_lo, bin_hi,
-                           stage_tf);
+                           stage_tf, err, (volatile uint32_t*)err_host);
 }
 
 void launch_acc_init(const Acc& acc, uint32_t W, int M, cudaStream_t st) {
