@@ -324,6 +324,15 @@ __device__ __forceinline__ dvl_vertex make_vertex(uint32_t cnt, uint32_t mn, uin
   return v;
 }
 
+// The same sum (mod 2^64) from three 32-bit warp reductions of 22-bit chunks (each chunk
+// sum < 2^27: no overflow), every lane gets it.
+__device__ __forceinline__ unsigned long long warp_sum_u64_redux(unsigned long long v) {
+  const uint32_t c0 = __reduce_add_sync(0xffffffffu, (uint32_t)v & 0x3fffffu);
+  const uint32_t c1 = __reduce_add_sync(0xffffffffu, (uint32_t)(v >> 22) & 0x3fffffu);
+  const uint32_t c2 = __reduce_add_sync(0xffffffffu, (uint32_t)(v >> 44));
+  return (unsigned long long)c0 + ((unsigned long long)c1 << 22) + ((unsigned long long)c2 << 44);
+}
+
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
