@@ -408,6 +408,24 @@ def run_native(args, rank, world, local):
         polylines(W, out=res)   # host output: synchronises
         e2e_times.append(time.perf_counter() - t0)
     e2e_ms = 1e3 * sum(e2e_times) / len(e2e_times)
+
+    # ---- brushing / linking: 2^22 random point queries on the device
+    locate = None
+    if world == 1:
+        g = torch.Generator(device=dev).manual_seed(11)
+        qp = torch.randint(0, 1 << int(info["bits"]), (1 << 22, 3), generator=g, device=dev,
+                           dtype=torch.int32)
+        ctx.locate(qp)
+        torch.cuda.synchronize()
+        la, lb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lst = torch.cuda.ExternalStream(ctx.stream)
+        la.record(lst)
+        for _ in range(5):
+            ctx.locate(qp)
+        lb.record(lst)
+        torch.cuda.synchronize()
+        lms = la.elapsed_time(lb) / 5
+        locate = {"queries": 1 << 22, "ms": lms, "gpoints_per_s": (1 << 22) / (lms / 1e3) / 1e9}
     if dist:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -469,6 +487,7 @@ def run_native(args, rank, world, local):
         "e2e": {"value": n_global / (e2e_ms / 1e3) / 1e9, "unit": "Gcells/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": N * 16, "d2h_bytes_per_step": M * W * 32},
         "roofline": roof,
+        "locate": locate,
         "paper_context": {"value": 0.61, "unit": "Gcells/s", "gpu": "NVIDIA A6000",
                           "workload": "Molecular Cloud, 35.8 M cells x 4 fields, 4 AMR levels",
                           "derived_from": "Table 1 (PAPER.md lines 390-395): 58.6 ms per TF edit",

@@ -109,6 +109,17 @@ typedef struct {
     int32_t reserved;
 } dvl_info_t;
 
+/* Point location for brushing and linking: for each of npts
+ * integer points xyz[3 * i + 0..2] of the logical grid, the index in curve order (global:
+ * with the shard's offset; the order of dvl_get_sorted and of the bin ranges) of the cell
+ * whose 2^L cube contains it, or -1 if no cell of this context does (a gap, or outside
+ * [0, 2^b)^3).  A pixel brush [x0, x1] selects the cells [lo[x0], hi[x1]] of
+ * dvl_get_bin_ranges, so a point is inside the brushed region iff its index is in that
+ * range.  xyz and cell are in memory space `where` (host: synchronises).  Errors: STATE,
+ * INVAL, NOMEM, CUDA. */
+dvl_status dvl_locate(dvl_ctx *ctx, uint64_t npts, const uint32_t *xyz, int64_t *cell,
+                      dvl_mem where);
+
 /* Milliseconds of the last build / update / get_polylines, measured with CUDA events on
  * the context stream (only with DVL_FLAG_TIMING; otherwise all zero). */
 typedef struct {

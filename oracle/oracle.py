@@ -276,3 +276,23 @@ def update(B: Built, tfs, W: int, P: float = 1.0, eps: float = 0.025,
     lib().or_reduce(B.n, M, N, _p(B.scal_s), _p(tfs), _p(lo), _p(inv), W, _p(b1), _p(b2),
                     _p(out), _p(blo), _p(bhi))
     return Update(mv, s, f, q, Q, Qtot, b1, b2, out, blo, bhi)
+
+
+# ------------------------------------------------------------------ brushing / linking
+def locate(lower, level, B: Built, pts) -> np.ndarray:
+    """Brushing and linking: for each integer point of the
+    logical grid, the curve-order index (the position in B.codes) of the cell whose 2^L cube
+    [lower, lower + 2^L) contains it, -1 if none.  The plain definition: a containment test
+    against every cell (cells are disjoint, O4, so at most one matches)."""
+    lower = np.asarray(lower, dtype=np.int64).reshape(-1, 3)
+    w = (np.int64(1) << np.asarray(level, dtype=np.int64))[:, None]
+    rank = np.empty(B.n, np.int64)
+    rank[B.perm.astype(np.int64)] = np.arange(B.n, dtype=np.int64)   # input id -> curve order
+    pts = np.asarray(pts, dtype=np.int64).reshape(-1, 3)
+    out = np.full(len(pts), -1, np.int64)
+    for i, p in enumerate(pts):
+        hit = np.nonzero(np.all((lower <= p) & (p < lower + w), axis=1))[0]
+        assert len(hit) <= 1
+        if len(hit):
+            out[i] = rank[hit[0]]
+    return out

@@ -1339,6 +1339,49 @@ dvl_status dvl_get_prefix(dvl_ctx* ctx, uint64_t* Q, dvl_mem where) {
   return DVL_OK;
 }
 
+dvl_status dvl_locate(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t* cell,
+                      dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "dvl_locate before dvl_build");
+    return DVL_E_STATE;
+  }
+  if ((npts && (!xyz || !cell)) || (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE)) {
+    set_err(ctx, "dvl_locate: null buffer or bad memory space");
+    return DVL_E_INVAL;
+  }
+  if (npts == 0) return DVL_OK;
+  uint32_t* dx = nullptr;
+  int64_t* dc = nullptr;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const Dataset& d = ctx->ds;
+    const uint32_t* px = xyz;
+    int64_t* pc = cell;
+    if (where == DVL_MEM_HOST) {
+      dx = dalloc<uint32_t>(ctx, 3 * (size_t)npts);
+      dc = dalloc<int64_t>(ctx, (size_t)npts);
+      CK(cudaMemcpyAsync(dx, xyz, 12 * (size_t)npts, cudaMemcpyHostToDevice, ctx->stream));
+      px = dx;
+      pc = dc;
+    }
+    launch_locate(px, (int64_t)npts, d.b, ctx->d_t1, ctx->d_t2, ctx->nstates, d.keys, d.key_bytes,
+                  d.level_s, d.n, ctx->cell_offset, pc, ctx->stream);
+    CKLAUNCH();
+    if (where == DVL_MEM_HOST) {
+      CK(cudaMemcpyAsync(cell, dc, 8 * (size_t)npts, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  } catch (Fail& f) {
+    dfree(ctx, dx);
+    dfree(ctx, dc);
+    return f.s;
+  }
+  dfree(ctx, dx);
+  dfree(ctx, dc);
+  return DVL_OK;
+}
+
 dvl_status dvl_get_bin_ranges(dvl_ctx* ctx, uint32_t W, uint64_t* lo, uint64_t* hi,
                               dvl_mem where) {
   if (!ctx) return DVL_E_INVAL;

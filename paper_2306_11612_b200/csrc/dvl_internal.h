@@ -100,6 +100,10 @@ void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan&
                                unsigned long long* chunk_prefix, unsigned long long* qtot,
                                unsigned long long* meta, unsigned long long* meta2, int cmode,
                                cudaStream_t st);
+void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t1,
+                   const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
+                   const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
+                   cudaStream_t st);
 size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);
 cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds

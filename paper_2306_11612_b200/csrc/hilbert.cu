@@ -207,6 +207,80 @@ void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, 
         lower, level, n, b, passes, d_t1, d_t2, nstates, (unsigned long long*)keys, ids, hist);
 }
 
+// Point location (brushing / linking): the cell containing each integer point
+// of the logical grid, as its global index in curve order (-1: no cell contains it).  A
+// cell of level L covers the aligned 2^L cube, whose points the curve visits as one aligned
+// run of 8^L codes, so the point's code h lies in the run of the last cell with key <= h or
+// of the next one (whose centroid may come after h in its run): a binary search over the
+// sorted keys and two range checks.
+template <typename K>
+__global__ void __launch_bounds__(kBlock)
+locate_kernel(const uint32_t* __restrict__ xyz, int64_t npts, int b,
+              const uint16_t* __restrict__ t1g, const uint16_t* __restrict__ t2g, int nstates,
+              const K* __restrict__ keys, const uint8_t* __restrict__ level, int64_t n,
+              uint64_t cell_offset, int64_t* __restrict__ out) {
+  extern __shared__ uint16_t s_tab[];
+  uint16_t* s_t1 = s_tab;
+  uint16_t* s_t2 = s_tab + nstates * 8;
+  for (int i = threadIdx.x; i < nstates * 8; i += kBlock) s_t1[i] = t1g[i];
+  for (int i = threadIdx.x; i < nstates * 64; i += kBlock) s_t2[i] = t2g[i];
+  __syncthreads();
+  for (int64_t h = (int64_t)blockIdx.x * kBlock + threadIdx.x; h < npts;
+       h += (int64_t)gridDim.x * kBlock) {
+    const uint32_t x = xyz[3 * h], y = xyz[3 * h + 1], z = xyz[3 * h + 2];
+    int64_t res = -1;
+    if (n > 0 && ((x | y | z) >> b) == 0) {
+      int s = 0;
+      uint64_t code = 0;
+      int j = b - 1;
+      if (b & 1) {
+        int oct = (((x >> j) & 1) << 2) | (((y >> j) & 1) << 1) | ((z >> j) & 1);
+        uint16_t e = s_t1[s * 8 + oct];
+        code = e & 7;
+        s = e >> 3;
+        --j;
+      }
+      for (; j >= 1; j -= 2) {
+        uint16_t e = s_t2[s * 64 + two_levels(x, y, z, j)];
+        code = (code << 6) | (e & 63);
+        s = e >> 6;
+      }
+      // i = the number of keys <= code, minus 1
+      int64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)keys[mid] <= code) lo = mid + 1; else hi = mid;
+      }
+      for (int64_t c = lo - 1; c <= lo; ++c) {
+        if (c < 0 || c >= n) continue;
+        const uint64_t len = 1ull << (3 * level[c]);
+        const uint64_t start = (uint64_t)keys[c] & ~(len - 1);
+        if (code >= start && code - start < len) {
+          res = (int64_t)(cell_offset + (uint64_t)c);
+          break;
+        }
+      }
+    }
+    out[h] = res;
+  }
+}
+
+void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t1,
+                   const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
+                   const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
+                   cudaStream_t st) {
+  const size_t smem = (size_t)nstates * (8 + 64) * sizeof(uint16_t);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((npts + kBlock - 1) / kBlock, 4096));
+  if (key_bytes == 4)
+    locate_kernel<uint32_t><<<grid, kBlock, smem, st>>>(xyz, npts, b, d_t1, d_t2, nstates,
+                                                        (const uint32_t*)keys, level, n,
+                                                        cell_offset, out);
+  else
+    locate_kernel<unsigned long long><<<grid, kBlock, smem, st>>>(
+        xyz, npts, b, d_t1, d_t2, nstates, (const unsigned long long*)keys, level, n, cell_offset,
+        out);
+}
+
 __global__ void iota_kernel(uint32_t* v, int64_t n) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)

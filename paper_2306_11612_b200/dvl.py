@@ -29,7 +29,7 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
            "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
            "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
-           "dvl_shard_finish", "dvl_set_timing"]
+           "dvl_shard_finish", "dvl_set_timing", "dvl_locate"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -108,6 +108,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_shard_export_words": (u64, [P, u32]),
         "dvl_shard_reduce": (i32, [P, u32, P, i32, i32, P]),
         "dvl_shard_finish": (i32, [P, u32, P, P, i32]),
+        "dvl_locate": (i32, [P, u64, P, P, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -282,6 +283,29 @@ class Context:
         self._check(self._lib.dvl_get_bin_ranges(self._h, W, _ptr(lo), _ptr(hi), HOST),
                     "dvl_get_bin_ranges")
         return lo, hi
+
+    # ------------------------------------------------------------ brushing / linking
+    def locate(self, xyz):
+        """Global curve-order index of the cell containing each integer point (n, 3) of the
+        logical grid, -1 if none: numpy in -> numpy int64 out; a torch CUDA uint32/int32
+        tensor in -> torch CUDA int64 out."""
+        if _is_device(xyz):
+            import torch
+            xyz = xyz.contiguous()
+            out = torch.empty(xyz.numel() // 3, dtype=torch.int64, device=xyz.device)
+            self._check(self._lib.dvl_locate(self._h, out.numel(), _ptr(xyz), _ptr(out), DEVICE),
+                        "dvl_locate")
+            return out
+        xyz = np.ascontiguousarray(np.asarray(xyz, dtype=np.uint32).reshape(-1, 3))
+        out = np.empty(len(xyz), np.int64)
+        self._check(self._lib.dvl_locate(self._h, len(xyz), _ptr(xyz), _ptr(out), HOST), "dvl_locate")
+        return out
+
+    def brush(self, W: int, x0: int, x1: int):
+        """The cells (first, last) in curve order selected by brushing pixels x0..x1 of the
+        last polylines of width W."""
+        lo, hi = self.get_bin_ranges(W)
+        return int(lo[x0]), int(hi[x1])
 
     # ------------------------------------------------------------------ sharding
     def set_global_bits(self, bits: int):

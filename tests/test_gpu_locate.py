@@ -1,0 +1,99 @@
+"""GPU parity of point location (dvl_locate; brushing / linking) against the
+oracle's containment test: points inside cells, in gaps and outside the grid, for u32 and
+u64 keys, host and device buffers; and the brush of a pixel range selects exactly the cells
+of its bin ranges."""
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dvl():
+    import paper_2306_11612_b200 as m
+    m.load()
+    return m
+
+
+def octree(E, Lmax, seed, p=0.45, keep=1.0):
+    rng = np.random.default_rng(seed)
+    lower, level = synth.uniform_cells(E >> Lmax)
+    lower = (lower << np.uint32(Lmax)).astype(np.uint32)
+    level = np.full(len(level), Lmax, np.uint8)
+    for L in range(Lmax, 0, -1):
+        mask = (level == L) & (rng.random(len(level)) < p)
+        lower, level = synth.refine(lower, level, mask)
+    k = rng.random(len(level)) < keep
+    return lower[k], level[k]
+
+
+def points(E, n, seed, lower=None, level=None):
+    rng = np.random.default_rng(seed)
+    pts = [rng.integers(0, E, size=(n, 3))]
+    if lower is not None:   # cell corners
+        idx = rng.integers(0, len(level), size=n // 4)
+        w = (1 << level[idx].astype(np.int64))[:, None]
+        pts += [lower[idx].astype(np.int64), lower[idx].astype(np.int64) + w - 1]
+    pts.append(np.array([[E, 0, 0], [0, E + 5, 0], [2 ** 21 - 1] * 3]))
+    return np.concatenate(pts).astype(np.uint32)
+
+
+@pytest.mark.parametrize("E,Lmax,seed,keep", [(32, 3, 1, 1.0), (64, 4, 2, 0.7), (16, 2, 3, 0.5)])
+def test_locate_matches_oracle(dvl, E, Lmax, seed, keep):
+    import torch
+    lower, level = octree(E, Lmax, seed, keep=keep)
+    scal = np.random.default_rng(seed).standard_normal((2, len(level))).astype(np.float32)
+    B = o.build(lower, level, scal)
+    ctx = dvl.Context(device=0)
+    ctx.build(lower, level, scal)
+    pts = points(E, 600, seed + 10, lower, level)
+    ref = o.locate(lower, level, B, pts)
+    assert np.array_equal(ctx.locate(pts), ref)
+    dev = ctx.locate(torch.from_numpy(pts.astype(np.int32)).cuda())
+    assert np.array_equal(dev.cpu().numpy(), ref)
+    ctx.close()
+
+
+def test_locate_u64_keys(dvl):
+    rng = np.random.default_rng(5)
+    E, n = 2 ** 14, 3000                        # 3b = 42 > 32: u64 keys
+    blocks = E >> 3
+    ids = rng.choice(blocks ** 3, size=n, replace=False)
+    lower = np.stack([ids % blocks, (ids // blocks) % blocks, ids // blocks ** 2], 1).astype(np.uint32) * 8
+    level = rng.integers(0, 4, size=n).astype(np.uint8)
+    scal = rng.standard_normal((1, n)).astype(np.float32)
+    B = o.build(lower, level, scal)
+    ctx = dvl.Context(device=0)
+    ctx.build(lower, level, scal)
+    assert ctx.info()["key_bytes"] == 8
+    w = (1 << level.astype(np.int64))[:, None]
+    pts = np.concatenate([lower.astype(np.int64), lower.astype(np.int64) + w - 1,
+                          rng.integers(0, E, size=(500, 3))]).astype(np.uint32)
+    assert np.array_equal(ctx.locate(pts), o.locate(lower, level, B, pts))
+    ctx.close()
+
+
+def test_brush_selects_the_bin_cells(dvl):
+    lower, level = octree(32, 3, 7)
+    scal = np.random.default_rng(7).standard_normal((4, len(level))).astype(np.float32)
+    B = o.build(lower, level, scal)
+    ctx = dvl.Context(device=0)
+    ctx.build(lower, level, scal)
+    W = 64
+    ctx.get_polylines(W)
+    lo, hi = ctx.get_bin_ranges(W)
+    first, last = ctx.brush(W, 10, 20)
+    assert (first, last) == (int(lo[10]), int(hi[20]))
+    # the brushed cells' centroids locate inside the range, the others outside
+    half = ((1 << level.astype(np.int64)) >> 1)[:, None]
+    cent = (lower.astype(np.int64) + half).astype(np.uint32)
+    k = ctx.locate(cent)
+    rank = np.empty(B.n, np.int64)
+    rank[B.perm.astype(np.int64)] = np.arange(B.n)
+    assert np.array_equal(k, rank)
+    inside = (k >= first) & (k <= last)
+    assert inside.sum() == last - first + 1
+    ctx.close()
