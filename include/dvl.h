@@ -172,6 +172,14 @@ dvl_status dvl_build(dvl_ctx *ctx, uint64_t n, const uint32_t *lower_xyz, const 
  * ceil(Lmax * P) > 100, fp32 weight overflow, reading A29). */
 dvl_status dvl_set_params(dvl_ctx *ctx, float P, float eps, dvl_maxv_mode mode);
 
+/* The level factor of the importance (Eq. 3): the cell width, f = (V/maxV 2^L)^P
+ * (default), or "another sensible choice ... by their volume", f =
+ * (V/maxV 2^3L)^P; the shift s becomes 61 - ceil(log2 n) - ceil(3 Lmax P).  Takes effect
+ * immediately (weights recomputed).  Errors: INVAL, RANGE (after a build: ceil(3 Lmax P) >
+ * 100). */
+typedef enum { DVL_SCALE_WIDTH = 0, DVL_SCALE_VOLUME = 1 } dvl_level_scale;
+dvl_status dvl_set_level_scale(dvl_ctx *ctx, dvl_level_scale scale);
+
 /* Normalisation domain [lo, hi] of one member (reading O6/A7): t =
  * clamp((v - lo) * inv, 0, 1) with inv = hi > lo ? 1/(hi - lo) : 0.  Default after a
  * build: the member's finite data range.  Errors: STATE (before build), INVAL (member

@@ -248,8 +248,12 @@ def maxv(B: Built, tfs: np.ndarray, lo, inv, mode: str = "conservative") -> floa
 
 
 def update(B: Built, tfs, W: int, P: float = 1.0, eps: float = 0.025,
-           mode: str = "conservative", domain=None, n_global: int | None = None) -> Update:
-    """One TF edit + polyline extraction: U0-U5 (Eq. 1, 3, 4)."""
+           mode: str = "conservative", domain=None, n_global: int | None = None,
+           scale: str = "width") -> Update:
+    """One TF edit + polyline extraction: U0-U5 (Eq. 1, 3, 4).  scale="volume":
+    the cell size enters Eq. 3 as the cell volume (2^L)^3 = 2^3L instead of the width 2^L,
+    "another sensible choice"; O10/O11 then see the level 3L."""
+    c = {"width": 1, "volume": 3}[scale]
     tfs = np.ascontiguousarray(np.asarray(tfs, dtype=np.float32))
     if tfs.ndim == 2:
         tfs = np.repeat(tfs[None], B.M, axis=0)
@@ -257,11 +261,12 @@ def update(B: Built, tfs, W: int, P: float = 1.0, eps: float = 0.025,
     assert M == B.M and tfs.shape[2] == 4
     lo, _, inv = domains(B, domain)
     mv = maxv(B, tfs, lo, inv, mode)
-    s = shift(B.n if n_global is None else n_global, B.Lmax, P)
+    s = shift(B.n if n_global is None else n_global, c * B.Lmax, P)
     alpha = np.ascontiguousarray(tfs[:, :, 3])
     f = np.empty(B.n, np.float32)
     q = np.empty(B.n, np.uint64)
-    lib().or_weights(B.n, M, N, _p(B.level_s), _p(B.scal_s), _p(alpha), _p(lo), _p(inv),
+    lev = np.ascontiguousarray((B.level_s.astype(np.int32) * c).astype(np.uint8))
+    lib().or_weights(B.n, M, N, _p(lev), _p(B.scal_s), _p(alpha), _p(lo), _p(inv),
                      mv, P, eps, s, _p(f), _p(q))
     Q = np.empty(B.n, np.uint64)
     Qtot = int(lib().or_prefix(B.n, _p(q), _p(Q)))

@@ -108,6 +108,7 @@ struct dvl_ctx {
   int launches = 0;
   int num_sms = 148;
   int acc_par = 0;                        // which lo / hi copy the next call uses
+  bool volume = false;                    // dvl_set_level_scale: weights by cell volume
   bool edit_cache = true;                 // DVL_EDIT_CACHE=0: every edit reads every member
   int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
@@ -251,6 +252,9 @@ bool smem_tab_ok(const dvl_ctx* ctx) {
   return (size_t)ctx->ds.M * ctx->N * sizeof(float2) <= 64 * 1024;
 }
 
+// the level factor of Eq. 3: 1 (cell width 2^L) or 3 (cell volume 2^3L)
+int lscale(const dvl_ctx* ctx) { return ctx->volume ? 3 : 1; }
+
 UpdParams upd_params(dvl_ctx* ctx) {
   UpdParams p{};
   const Dataset& d = ctx->ds;
@@ -268,6 +272,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.pw = pow_params(ctx->P);
   p.scale = pow2f(ctx->shift);
   p.shift = ctx->shift;
+  p.lscale = lscale(ctx);
   p.offset = 0;
   p.l2_keep = ctx->l2_keep;
   p.prod_sleep = ctx->prod_sleep;
@@ -285,7 +290,7 @@ int lmax_eff(const dvl_ctx* ctx) {
 // O11: s = 61 - ceil(log2 n) - ceil(Lmax P), over the whole (possibly sharded) dataset
 int compute_shift(dvl_ctx* ctx) {
   const uint64_t n = ctx->sharded ? ctx->n_global : (uint64_t)ctx->ds.n;
-  return 61 - ceil_log2_u64(n) - ceil_lmax_p(lmax_eff(ctx), ctx->P);
+  return 61 - ceil_log2_u64(n) - ceil_lmax_p(lscale(ctx) * lmax_eff(ctx), ctx->P);
 }
 
 void upload_domains(dvl_ctx* ctx) {
@@ -726,7 +731,7 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     CK(cudaStreamSynchronize(st));
     if (h_ing.err & kErrInval) fail(ctx, DVL_E_INVAL, "a cell has L > 20 or a lower corner not a multiple of 2^L");
     if (h_ing.extent > (1ull << 21)) fail(ctx, DVL_E_RANGE, "logical extent E > 2^21");
-    if (ceil_lmax_p((int)h_ing.lmax, ctx->P) > 100)
+    if (ceil_lmax_p(lscale(ctx) * (int)h_ing.lmax, ctx->P) > 100)
       fail(ctx, DVL_E_RANGE, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
     d.n = nn;
     d.M = M;
@@ -893,13 +898,36 @@ dvl_status dvl_set_params(dvl_ctx* ctx, float P, float eps, dvl_maxv_mode mode) 
     set_err(ctx, "bad maxV mode");
     return DVL_E_INVAL;
   }
-  if (ctx->built && ceil_lmax_p(lmax_eff(ctx), P) > 100) {
+  if (ctx->built && ceil_lmax_p(lscale(ctx) * lmax_eff(ctx), P) > 100) {
     set_err(ctx, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
     return DVL_E_RANGE;
   }
   ctx->P = P;
   ctx->eps = eps;
   ctx->mode = mode;
+  if (ctx->built) {
+    try {
+      CK(cudaSetDevice(ctx->device));
+      run_weights(ctx, false, nullptr);
+    } catch (Fail& f) {
+      return f.s;
+    }
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_set_level_scale(dvl_ctx* ctx, dvl_level_scale scale) {
+  if (!ctx) return DVL_E_INVAL;
+  if (scale != DVL_SCALE_WIDTH && scale != DVL_SCALE_VOLUME) {
+    set_err(ctx, "bad level scale");
+    return DVL_E_INVAL;
+  }
+  const int c = scale == DVL_SCALE_VOLUME ? 3 : 1;
+  if (ctx->built && ceil_lmax_p(c * lmax_eff(ctx), ctx->P) > 100) {
+    set_err(ctx, "ceil(c Lmax P) > 100 (fp32 weight overflow)");
+    return DVL_E_RANGE;
+  }
+  ctx->volume = scale == DVL_SCALE_VOLUME;
   if (ctx->built) {
     try {
       CK(cudaSetDevice(ctx->device));
@@ -1092,7 +1120,7 @@ dvl_status dvl_set_shard(dvl_ctx* ctx, const dvl_shard_info* info) {
     set_err(ctx, "inconsistent shard description");
     return DVL_E_INVAL;
   }
-  if (ceil_lmax_p(info->lmax_global, ctx->P) > 100) {
+  if (ceil_lmax_p(lscale(ctx) * (int)info->lmax_global, ctx->P) > 100) {
     set_err(ctx, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
     return DVL_E_RANGE;
   }

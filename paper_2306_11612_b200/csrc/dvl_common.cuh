@@ -63,6 +63,7 @@ struct UpdParams {
   PowParams pw;
   float scale;             // 2^s
   int shift;               // s
+  int lscale;              // 1: f scales by the cell width 2^L (Eq. 3); 3: by its volume 2^3L
   uint64_t offset;         // global prefix before this device's cells (sharding, host part)
   const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
   int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last

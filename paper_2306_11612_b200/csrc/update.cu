@@ -293,7 +293,7 @@ __device__ __forceinline__ void cell_weights(const UpdParams& p, const float2* t
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     float V = __fsub_rn(amax[i], amin[i]);
-    float f = importance(V, maxv, L[i], p.eps, p.pw);
+    float f = importance(V, maxv, L[i] * p.lscale, p.eps, p.pw);
     q[i] = (c0 + i < p.n) ? __float2ull_rz(__fmul_rn(f, p.scale)) : 0ull;
   }
 }

@@ -29,7 +29,7 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
            "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
            "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
-           "dvl_shard_finish", "dvl_set_timing", "dvl_locate"]
+           "dvl_shard_finish", "dvl_set_timing", "dvl_locate", "dvl_set_level_scale"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -109,6 +109,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_shard_reduce": (i32, [P, u32, P, i32, i32, P]),
         "dvl_shard_finish": (i32, [P, u32, P, P, i32]),
         "dvl_locate": (i32, [P, u64, P, P, i32]),
+        "dvl_set_level_scale": (i32, [P, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -210,6 +211,11 @@ class Context:
                                  DEVICE if dev else HOST)
         self._check(st, "dvl_build")
         self.M, self.n = M, n
+
+    def set_level_scale(self, scale: str = "width"):
+        """Eq. 3's level factor: "width" (2^L, default) or "volume" (2^3L)."""
+        self._check(self._lib.dvl_set_level_scale(self._h, {"width": 0, "volume": 1}[scale]),
+                    "dvl_set_level_scale")
 
     def set_params(self, P: float = 1.0, eps: float = 0.025, mode: str = "conservative"):
         self._check(self._lib.dvl_set_params(self._h, P, eps, MAXV_MODES[mode]), "dvl_set_params")

@@ -71,10 +71,12 @@ def tfs_for(M, N, seed, same=False):
 
 
 def run_gpu(dvl, lower, level, scal, tfs, W, P=1.0, eps=0.025, mode="conservative", domain=None,
-            generic=False):
+            generic=False, scale="width"):
     ctx = make_ctx(dvl, generic)
     ctx.build(lower, level, scal)
     ctx.set_params(P, eps, mode)
+    if scale != "width":
+        ctx.set_level_scale(scale)
     N = tfs.shape[1]
     if N != 256:
         ctx.reset_tfs(N)
@@ -168,6 +170,16 @@ def test_params(dvl, P, eps, path):
     scal = scalars(len(level), 4, 12)
     tfs = tfs_for(4, 64, 13)
     parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps, generic=path == "generic")
+
+
+@pytest.mark.parametrize("P", [0.5, 1.0, 2.0])
+@pytest.mark.parametrize("path", PATHS)
+def test_volume_scaled_importance(dvl, P, path):
+    """f = (V/maxV 2^3L)^P, the cell-volume variant of Eq. 3."""
+    lower, level = octree(32, 3, 90)
+    scal = scalars(len(level), 4, 91)
+    parity(dvl, lower, level, scal, tfs_for(4, 256, 92), 700, generic=path == "generic", P=P,
+           scale="volume")
 
 
 @pytest.mark.parametrize("mode", ["conservative", "per_entry", "exact"])
