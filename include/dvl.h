@@ -46,7 +46,7 @@ typedef enum {
     DVL_E_DEGENERATE = 5, /* sum of all fixed-point weights is 0 (only with eps = 0) */
     DVL_E_NOMEM = 6,      /* device or pinned host allocation failed */
     DVL_E_CUDA = 7,       /* a CUDA runtime error; text in dvl_last_error */
-    DVL_E_NCCL = 8        /* reserved for collective failures */
+    DVL_E_NCCL = 8        /* a collective failed (or libnccl.so.2 is missing); text in dvl_last_error */
 } dvl_status;
 
 typedef enum { DVL_MEM_HOST = 0, DVL_MEM_DEVICE = 1 } dvl_mem;
@@ -240,6 +240,17 @@ dvl_status dvl_shard_total(dvl_ctx *ctx, uint64_t *total_dev);
 
 /* Number of int64 words of the accumulator export for width W: 2 (W + M W) + 3 M W. */
 uint64_t dvl_shard_export_words(dvl_ctx *ctx, uint32_t W);
+
+/* The context's own NCCL communicator over the shards (NCCL over NVLink, loaded
+ * at run time from libnccl.so.2).  dvl_nccl_unique_id writes a 128-byte ncclUniqueId (call
+ * on one rank, broadcast it); dvl_set_comm (on every rank, collectively: blocks until all
+ * ranks join) makes rank `rank` of `nranks`.  A sharded context (dvl_set_shard) with a
+ * communicator runs the whole sharded edit in dvl_get_polylines: all_gather of the Q totals,
+ * pass 2 with the global offset, the accumulator export and one grouped MAX + SUM all_reduce
+ * of it, the merged epilogue -- the same result as dvl_shard_total / _reduce / _finish with
+ * the caller's collectives, in one call.  Errors: INVAL, NCCL, CUDA. */
+dvl_status dvl_nccl_unique_id(void *id128);
+dvl_status dvl_set_comm(dvl_ctx *ctx, int nranks, int rank, const void *id128);
 
 /* Pass 2 of this shard (U3+U4) with the global scan offset and Qtot derived on the device
  * from totals_dev[nshards] (the gathered dvl_shard_total values, shard order), then export

@@ -109,6 +109,13 @@ struct dvl_ctx {
   int num_sms = 148;
   int acc_par = 0;                        // which lo / hi copy the next call uses
   bool volume = false;                    // dvl_set_level_scale: weights by cell volume
+  // dvl_set_comm: the context's own NCCL communicator over the shards; dvl_get_polylines
+  // then runs the sharded edit (both exchanges) itself
+  void* comm = nullptr;
+  int comm_ranks = 0, comm_rank = 0;
+  unsigned long long* d_totals = nullptr;   // [comm_ranks]
+  int64_t* d_export = nullptr;              // the accumulator export, merged in place
+  uint64_t export_cap = 0;
   bool edit_cache = true;                 // DVL_EDIT_CACHE=0: every edit reads every member
   int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
@@ -652,6 +659,7 @@ void dvl_destroy(dvl_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  nccl_comm_destroy(ctx->comm);
   free_dataset(ctx, ctx->ds);
   std::vector<void*> ps;
   for (auto& kv : ctx->live) ps.push_back(kv.first);
@@ -1026,6 +1034,41 @@ dvl_status dvl_reset_tfs(dvl_ctx* ctx, uint32_t N) {
   return DVL_OK;
 }
 
+dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev, int nshards,
+                            int shard, int64_t* export_dev);
+dvl_status dvl_shard_finish(dvl_ctx* ctx, uint32_t W, const int64_t* merged_dev, dvl_vertex* out,
+                            dvl_mem where);
+
+// dvl_get_polylines of a context with its own communicator: the sharded edit of SURVEY 8(e)
+// as one call -- all_gather of the Q totals, pass 2 with the global offset, the export, one
+// grouped MAX + SUM all_reduce of it, the merged epilogue -- all on the context stream.
+static dvl_status sharded_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem where) {
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const uint64_t words = dvl_shard_export_words(ctx, W);
+    if (words > ctx->export_cap) {
+      dfree(ctx, ctx->d_export);
+      ctx->d_export = dalloc<int64_t>(ctx, (size_t)words);
+      ctx->export_cap = words;
+    }
+    if (const char* e = nccl_gather_totals(ctx->comm, (const uint64_t*)ctx->d_qtot,
+                                           (uint64_t*)ctx->d_totals, ctx->stream))
+      fail(ctx, DVL_E_NCCL, std::string("all_gather of the totals: ") + e);
+  } catch (Fail& f) {
+    return f.s;
+  }
+  dvl_status s = dvl_shard_reduce(ctx, W, (const uint64_t*)ctx->d_totals, ctx->comm_ranks,
+                                  ctx->comm_rank, ctx->d_export);
+  if (s != DVL_OK) return s;
+  const uint64_t MW = (uint64_t)ctx->ds.M * W;
+  if (const char* e = nccl_merge_export(ctx->comm, ctx->d_export, 2 * (W + MW), 3 * MW,
+                                        ctx->stream)) {
+    set_err(ctx, std::string("merge of the exports: ") + e);
+    return DVL_E_NCCL;
+  }
+  return dvl_shard_finish(ctx, W, ctx->d_export, out, where);
+}
+
 dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem where) {
   if (!ctx) return DVL_E_INVAL;
 
@@ -1037,6 +1080,7 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     set_err(ctx, "W must be in [2, 65536] and out non-NULL");
     return DVL_E_INVAL;
   }
+  if (ctx->comm && ctx->sharded) return sharded_polylines(ctx, W, out, where);
   try {
     CK(cudaSetDevice(ctx->device));
     ensure_acc(ctx, W);
@@ -1161,6 +1205,38 @@ dvl_status dvl_shard_total(dvl_ctx* ctx, uint64_t* total_dev) {
   try {
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(total_dev, ctx->d_qtot, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_nccl_unique_id(void* id128) {
+  if (!id128) return DVL_E_INVAL;
+  return nccl_unique_id(id128) ? DVL_E_NCCL : DVL_OK;
+}
+
+dvl_status dvl_set_comm(dvl_ctx* ctx, int nranks, int rank, const void* id128) {
+  if (!ctx) return DVL_E_INVAL;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id128) {
+    set_err(ctx, "bad communicator arguments");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->comm) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      nccl_comm_destroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    void* c = nullptr;
+    if (const char* e = nccl_comm_init(&c, nranks, rank, id128))
+      fail(ctx, DVL_E_NCCL, std::string("ncclCommInitRank: ") + e);
+    dfree(ctx, ctx->d_totals);
+    ctx->d_totals = dalloc<unsigned long long>(ctx, (size_t)nranks);
+    ctx->comm = c;
+    ctx->comm_ranks = nranks;
+    ctx->comm_rank = rank;
   } catch (Fail& f) {
     return f.s;
   }

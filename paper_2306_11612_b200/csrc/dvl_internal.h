@@ -104,6 +104,14 @@ void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t
                    const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
                    const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
                    cudaStream_t st);
+// comm.cu: NCCL resolved at run time; each returns nullptr or an error text
+const char* nccl_unique_id(void* id128);
+const char* nccl_comm_init(void** comm, int nranks, int rank, const void* id128);
+void nccl_comm_destroy(void* comm);
+const char* nccl_gather_totals(void* comm, const uint64_t* total, uint64_t* totals,
+                               cudaStream_t st);
+const char* nccl_merge_export(void* comm, int64_t* buf, size_t max_words, size_t sum_words,
+                              cudaStream_t st);
 size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);
 cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds

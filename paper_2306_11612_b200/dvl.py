@@ -29,7 +29,8 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_get_prefix", "dvl_get_bin_ranges", "dvl_get_timings", "dvl_stream",
            "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
            "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
-           "dvl_shard_finish", "dvl_set_timing", "dvl_locate", "dvl_set_level_scale"]
+           "dvl_shard_finish", "dvl_set_timing", "dvl_locate", "dvl_set_level_scale",
+           "dvl_nccl_unique_id", "dvl_set_comm"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -110,6 +111,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_shard_finish": (i32, [P, u32, P, P, i32]),
         "dvl_locate": (i32, [P, u64, P, P, i32]),
         "dvl_set_level_scale": (i32, [P, i32]),
+        "dvl_nccl_unique_id": (i32, [P]),
+        "dvl_set_comm": (i32, [P, i32, i32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -314,6 +317,11 @@ class Context:
         return int(lo[x0]), int(hi[x1])
 
     # ------------------------------------------------------------------ sharding
+    def set_comm(self, nranks: int, rank: int, uid: bytes):
+        """Join the context's own NCCL communicator (collective over the ranks)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        self._check(self._lib.dvl_set_comm(self._h, nranks, rank, buf), "dvl_set_comm")
+
     def set_global_bits(self, bits: int):
         self._check(self._lib.dvl_set_global_bits(self._h, bits), "dvl_set_global_bits")
 
@@ -359,3 +367,11 @@ class Context:
         t = _Timings()
         self._check(self._lib.dvl_get_timings(self._h, ctypes.byref(t)), "dvl_get_timings")
         return {k: getattr(t, k) for k, _ in _Timings._fields_}
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (libnccl.so.2 loaded at run time by the library)."""
+    buf = ctypes.create_string_buffer(128)
+    if load().dvl_nccl_unique_id(buf) != 0:
+        raise DvlError("dvl_nccl_unique_id: libnccl.so.2 not available")
+    return buf.raw

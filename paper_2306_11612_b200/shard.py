@@ -64,7 +64,10 @@ def scan_offset(totals, rank: int):
 class ShardedContext:
     """A dvl Context that is one shard of a dataset distributed over the ranks of `group`."""
 
-    def __init__(self, ctx, group=None):
+    def __init__(self, ctx, group=None, native: bool = True):
+        """native: the context gets its own NCCL communicator (dvl_set_comm) and each
+        get_polylines is one library call that runs both exchanges itself; otherwise the
+        exchanges are torch.distributed collectives between the library's shard calls."""
         import torch
         import torch.distributed as dist
         self.ctx, self.group = ctx, group
@@ -73,6 +76,15 @@ class ShardedContext:
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self._total = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self._bufs = {}
+        self.native = False
+        if native and dist.get_backend(group) == "nccl":
+            from . import dvl as _dvl
+            uid = torch.zeros(128, dtype=torch.uint8, device=self.dev)
+            if self.rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(_dvl.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            ctx.set_comm(self.world, self.rank, bytes(uid.cpu().numpy().tobytes()))
+            self.native = True
 
     def describe(self, n_local: int, lmax_local: int, vmin, vmax):
         """After the local build: agree on offsets, n, Lmax and member ranges."""
@@ -92,6 +104,8 @@ class ShardedContext:
 
     def get_polylines(self, W: int, out=None):
         import torch
+        if self.native:   # both exchanges inside the library (one call)
+            return self.ctx.get_polylines(W, out=out)
         if W not in self._bufs:
             self._bufs[W] = torch.empty(self.ctx.shard_export_words(W), dtype=torch.int64,
                                         device=self.dev)

@@ -98,3 +98,35 @@ def test_sharded_equals_unsharded(dvl, G, generic, W):
     full.close()
     for k in ("count", "t_min", "t_max"):
         assert np.array_equal(one[k], out[k])
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_native_comm_single_rank(dvl, generic):
+    """The library's own NCCL path (dvl_set_comm + dvl_get_polylines of a sharded context,
+    both exchanges inside the call) with one rank: every output equals the unsharded
+    context bit for bit, over several edits (one rank is all NCCL allows on one GPU; the
+    multi-rank exchanges are the same collectives as the torch path above)."""
+    from paper_2306_11612_b200 import dvl as D
+    lower, level = octree(32, 3, 81)
+    M = 4
+    scal = np.random.default_rng(82).standard_normal((M, len(level))).astype(np.float32)
+    B = o.build(lower, level, scal)
+    tfs = np.stack([synth.random_tf(83 + m, 256, member=m) for m in range(M)])
+    plain = dvl.Context(device=0, generic=generic)
+    plain.build(lower, level, scal)
+    sh = dvl.Context(device=0, generic=generic)
+    sh.build(lower, level, scal)
+    sh.set_shard(0, B.n, B.Lmax, B.vmin, B.vmax)
+    sh.set_comm(1, 0, D.nccl_unique_id())
+    W = 512
+    for e in range(3):
+        for c in (plain, sh):
+            for m in range(M):
+                c.update_tf(m, tfs[m] if e == 0 else synth.tf_edit(4, e, 256, member=m))
+        a, b = plain.get_polylines(W), sh.get_polylines(W)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), e
+        la, ha = plain.get_bin_ranges(W)
+        lb, hb = sh.get_bin_ranges(W)
+        assert np.array_equal(la, lb) and np.array_equal(ha, hb)
+    plain.close()
+    sh.close()
