@@ -1265,11 +1265,17 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     CK(cudaSetDevice(ctx->device));
     ensure_acc(ctx, W);
     Dataset& d = ctx->ds;
-    launch_shard_offsets((const unsigned long long*)totals_dev, nshards, shard, ctx->d_offset,
-                         ctx->d_qtot_glob, ctx->stream);
-    CKLAUNCH();
     UpdParams p = upd_params(ctx);
-    p.offset_dev = ctx->d_offset;
+    if (d.tma) {   // pass 2 sums the offset and Qtot from the totals itself
+      p.shard_totals = (const unsigned long long*)totals_dev;
+      p.nshards = nshards;
+      p.shard = shard;
+    } else {
+      launch_shard_offsets((const unsigned long long*)totals_dev, nshards, shard, ctx->d_offset,
+                           ctx->d_qtot_glob, ctx->stream);
+      CKLAUNCH();
+      p.offset_dev = ctx->d_offset;
+    }
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)

@@ -66,6 +66,10 @@ struct UpdParams {
   int lscale;              // 1: f scales by the cell width 2^L (Eq. 3); 3: by its volume 2^3L
   uint64_t offset;         // global prefix before this device's cells (sharding, host part)
   const unsigned long long* offset_dev;   // ... and its device part (nullptr: 0)
+  // sharded pass 2 (TMA path): the gathered Q totals of all shards; the scan offset of this
+  // shard and the global Qtot are summed from them inside the kernel (nullptr: not sharded)
+  const unsigned long long* shard_totals;
+  int nshards, shard;
   int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
   uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
   int dbg;                 // timing experiments only: 1 skip pass-2 folds, 2 skip pass-1 weights
