@@ -117,7 +117,6 @@ struct dvl_ctx {
   int64_t* d_export = nullptr;              // the accumulator export, merged in place
   uint64_t export_cap = 0;
   bool edit_cache = true;                 // DVL_EDIT_CACHE=0: every edit reads every member
-  int l2_keep = 0;                        // pass-1 L2 policy (see UpdParams)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
   int stages_override = 0;
   int dbg = 0;                // experiment: pass-2 ring depth
@@ -281,7 +280,6 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.shift = ctx->shift;
   p.lscale = lscale(ctx);
   p.offset = 0;
-  p.l2_keep = ctx->l2_keep;
   p.prod_sleep = ctx->prod_sleep;
   p.dbg = ctx->dbg;
   p.cmin = d.cmin;
@@ -377,12 +375,6 @@ void ensure_plan(dvl_ctx* ctx) {
   int G1 = std::min(pl.tiles1, ctx->num_sms * bps1);
   pl.tpc1 = (pl.tiles1 + G1 - 1) / G1;
   G1 = (pl.tiles1 + pl.tpc1 - 1) / pl.tpc1;
-  // pass-1 tile order for L2 reuse by pass 2 (l2_keep: pass 1 leaves its reads in L2)
-  pl.order1 = 0;   // (the D3 records need pass 1 in tile order)
-  if (false) {
-    const int64_t c2 = (int64_t)pl.tpc * T2;           // cells of a pass-2 chunk
-    pl.order1 = (c2 % T1 == 0 && (pl.tpc1 * T1) % c2 == 0) ? (int)(c2 / T1) : -1;
-  }
   if (G1 + 1 > d.chunk_cap) {
     unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
     unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);
@@ -616,7 +608,7 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
       prepared = true;
     }
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    if (const char* e = getenv("DVL_L2_KEEP")) ctx->l2_keep = atoi(e);   // experiment knobs
+    // experiment knobs
     if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
     if (const char* e = getenv("DVL_STAGES2")) ctx->stages_override = atoi(e);
     if (const char* e = getenv("DVL_DBG")) ctx->dbg = atoi(e);

@@ -70,7 +70,6 @@ struct UpdParams {
   // shard and the global Qtot are summed from them inside the kernel (nullptr: not sharded)
   const unsigned long long* shard_totals;
   int nshards, shard;
-  int l2_keep;             // pass-1 loads: 0 evict_first, 1 evict_normal, 2 evict_last
   uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
   int dbg;                 // timing experiments only: 1 skip pass-2 folds, 2 skip pass-1 weights
   // edit cache (repeated TF edits of one member): per cell the min / max of the alpha bits
@@ -93,8 +92,6 @@ struct TmaPlan {
   int stages1;
   uint32_t stage_bytes1;  // M * T1 * 4 + T1, rounded up to 128
   uint32_t tab_bytes;     // pass 1: alpha table in shared memory (0: read through L1)
-  int order1;             // pass 1 tile order: 0 in order; k > 0: its chunk is k-tile groups
-                          // (one per pass-2 chunk) walked backwards in lockstep; -1 backwards
 };
 
 // Division by the pixel count W of one get_polylines call (2 <= W <= 2^16) with a
