@@ -51,6 +51,8 @@ struct Dataset {
   unsigned long long* meta2 = nullptr;          // n_pad / 128: the warp's running q sum in its
                                                 // pass-1 chunk before the warp tile's tile
   void* agg = nullptr;                          // D3: per warp tile and member t statistics
+  unsigned long long* blist = nullptr;          // 2 x n_pad / 128: listed boundary warp tiles
+  uint32_t* bctr = nullptr;                     // their count + done counter (self-resetting)
   // edit cache (TMA path, M >= 3): per cell the min / max of the alpha bits of the members
   // other than cache_member, valid while their TFs and the domains stay as they were
   uint32_t* cmin = nullptr;
@@ -205,7 +207,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
   void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
-                d.tile_meta, d.meta2, d.agg, d.cmin, d.cmax};
+                d.tile_meta, d.meta2, d.agg, d.cmin, d.cmax, d.blist, d.bctr};
   for (void* p : ps) dfree(ctx, p);
   d = Dataset();
 }
@@ -843,6 +845,9 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
       d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
       d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
       d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
+      d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
+      d.bctr = dalloc<uint32_t>(ctx, 2);
+      CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), st));
     }
     CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
@@ -1084,7 +1089,8 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, ctx->stream);
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
+                          ctx->num_sms, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
@@ -1272,7 +1278,8 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     tic(ctx, PH_BREDUCE);
     if (d.tma)
       launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, ctx->stream);
+                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
+                          ctx->num_sms, ctx->stream);
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);

@@ -116,10 +116,13 @@ size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);
 cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds
 void launch_agg_build(const UpdParams& p, void* agg, int64_t nwt, int num_sms, cudaStream_t st);
+// blist / bctr (2 x n_pad / 128 u64, 2 u32 zeroed once): the boundary-tile list, used when
+// the pixels outnumber agg_reduce's warps (then a bin_boundary launch follows)
 void launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned long long* chunk_prefix,
                        const unsigned long long* qtot, uint32_t W, const Acc& acc,
                        uint64_t cell_offset, uint32_t* err, const unsigned long long* meta,
-                       const unsigned long long* meta2, const void* agg, cudaStream_t st);
+                       const unsigned long long* meta2, const void* agg, unsigned long long* blist,
+                       uint32_t* bctr, int num_sms, cudaStream_t st);
 void launch_q_export_tma(bool smem_tab, const UpdParams& p, const TmaPlan& plan, int grid,
                          const unsigned long long* chunk_prefix, const unsigned long long* qtot,
                          uint32_t* err, unsigned long long* q_out, const unsigned long long* meta,
