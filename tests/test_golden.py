@@ -39,3 +39,14 @@ def test_index_range(case):
 @pytest.mark.parametrize("case", G["hilbert"], ids=lambda c: f'{c["cite"]}-{c["b"]}')
 def test_hilbert(case):
     assert int(o.hilbert_encode([case["xyz"]], case["b"])[0]) == case["h"]
+
+
+def test_hilbert_vectors_reproduced_by_independent_generator():
+    """The committed Hilbert vectors are exactly what tests/golden/gen_hilbert.py computes
+    from Skilling's decoder alone (no oracle code), so they are reproducible."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "gen_hilbert", os.path.join(os.path.dirname(__file__), "golden", "gen_hilbert.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    assert gen.generate() == G["hilbert"]

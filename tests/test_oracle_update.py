@@ -329,6 +329,8 @@ def test_reduce_matches_rational_bruteforce(seed):
             A = tf[m, :, 3]
             assert v["y"] == f32(o.sample(A, float(v["t_mean"])))
             assert v["r"] == f32(o.sample(tf[m, :, 0], float(v["t_mean"])))
+            assert v["g"] == f32(o.sample(tf[m, :, 1], float(v["t_mean"])))
+            assert v["b"] == f32(o.sample(tf[m, :, 2], float(v["t_mean"])))
     assert rng_n == B.n
 
 
@@ -420,3 +422,100 @@ def test_eight_cell_ensemble_exact_and_r1():
     assert U.maxV == 0.0
     assert U.b1.tolist() == [0, 0, 1, 1, 2, 2, 3, 3] and U.b1.tolist() == U.b2.tolist()
     assert U.vertices[1]["t_mean"].tolist() == [0.25, 0.5, 0.375, 0.25]
+
+
+# ------------------------------------- maxV restricted to the data's TF index range [i, j]
+def _index_range_fixture():
+    """P:272-278 ("ranges [i_m, j_m] of the transfer-function indices ... iterate only over
+    the transfer function values present in the data").  Two members on a shared domain
+    [0, 8] with N = 9 entries (inv = 1/8 exactly, so t (N-1) = v): member 0 holds values in
+    [2, 3] -> [i_0, j_0] = [2, 3]; member 1 in [4, 5] -> [4, 5]; so [i, j] = [2, 5].  The
+    alpha extremes of both tables (1.0 and 0.0) lie outside [2, 5]."""
+    n = 8
+    lower = np.stack([np.arange(n), np.zeros(n), np.zeros(n)], 1).astype(np.uint32)
+    m0 = np.array([2.0, 3.0, 2.5, 2.0, 3.0, 2.25, 2.75, 2.0], f32)
+    m1 = np.array([4.0, 5.0, 4.5, 5.0, 4.0, 4.25, 4.75, 4.0], f32)
+    B = o.build(lower, np.zeros(n, np.uint8), np.stack([m0, m1]))
+    tf = np.zeros((2, 9, 4), f32)
+    tf[0, :, 3] = [1.0, 0.9, 0.30, 0.50, 0.40, 0.60, 0.0, 0.1, 1.0]
+    tf[1, :, 3] = [0.0, 0.05, 0.20, 0.35, 0.70, 0.45, 1.0, 0.8, 0.0]
+    tf[:, :, 0], tf[:, :, 1], tf[:, :, 2] = 0.1, 0.2, 0.3
+    return B, tf
+
+
+def test_maxv_uses_only_the_data_index_range():
+    """Hand-computed over a in [2, 5] (P:272-284): R2 = max{.30,.50,.40,.60,.20,.35,.70,.45}
+    - min{...} = 0.70 - 0.20; R1 = max_a |alpha_0[a] - alpha_1[a]| = |0.40 - 0.70| (a = 4).
+    Over the whole tables both would be 1.0 (a = 0 and the 0/1 entries), and with member
+    0's range alone ([2, 3]) R2 would be 0.50 - 0.20 -- so a dropped [i, j] restriction or a
+    wrong min/max over the members fails here."""
+    B, tf = _index_range_fixture()
+    lo, _, inv = o.domains(B, [[0.0, 8.0]])
+    assert inv[0] == f32(0.125)
+    assert o.index_range(float(B.vmin[0]), float(B.vmax[0]), 0.0, float(inv[0]), 9) == (2, 3)
+    assert o.index_range(float(B.vmin[1]), float(B.vmax[1]), 0.0, float(inv[1]), 9) == (4, 5)
+    r2 = o.maxv(B, tf, lo, inv, "conservative")
+    r1 = o.maxv(B, tf, lo, inv, "per_entry")
+    assert r2 == f32(f32(0.70) - f32(0.20))
+    assert r1 == f32(f32(0.70) - f32(0.40))
+    ex = o.maxv(B, tf, lo, inv, "exact")
+    assert r2 >= ex
+    # the importance follows (Eq. 3, P = 1, L = 0): the cell with member 0 at 2.0 (alpha
+    # 0.30) and member 1 at 4.0 (alpha 0.70) has V = 0.70 - 0.30 and f = V / R2
+    U = o.update(B, tf, 8, P=1.0, eps=0.025, domain=[[0.0, 8.0]])
+    k = int(np.nonzero(B.perm == 0)[0][0])
+    V = f32(f32(0.70) - f32(0.30))
+    assert U.maxV == r2 and U.f[k] == f32(V / r2)
+
+
+def test_index_range_floor_and_ceil_between_knots():
+    """P:272-275: i = floor of the lower data position, j = ceil of the upper one (S:196-198);
+    positions between knots widen the range outward; j is capped at N - 1."""
+    inv = o.domain_inv(0.0, 8.0)
+    assert o.index_range(2.5, 3.5, 0.0, inv, 9) == (2, 4)
+    assert o.index_range(2.0, 3.0, 0.0, inv, 9) == (2, 3)
+    assert o.index_range(-1.0, 9.0, 0.0, inv, 9) == (0, 8)
+    assert o.index_range(7.9, 8.0, 0.0, inv, 9) == (7, 8)
+
+
+def test_maxv_restricted_range_r2_bounds_exact_random():
+    """R2 over [i, j] is still an upper bound of the exact max(V_h) (reading A8) when the
+    domains are wider than the data, so [i, j] is a strict sub-range of [0, N-1]."""
+    for seed in range(20):
+        rng = np.random.default_rng(700 + seed)
+        M, n, N = int(rng.integers(2, 5)), 300, int(rng.integers(5, 200))
+        lower = np.stack([np.arange(n), np.zeros(n), np.zeros(n)], 1).astype(np.uint32)
+        a, w = rng.uniform(1, 3, (M, 1)), rng.uniform(0.5, 2, (M, 1))
+        scal = (a + w * rng.random((M, n))).astype(f32)
+        B = o.build(lower, np.zeros(n, np.uint8), scal)
+        lo, _, inv = o.domains(B, [[0.0, 6.0]])
+        tf = rng.random((M, N, 4)).astype(f32)
+        ex = o.maxv(B, tf, lo, inv, "exact")
+        r2 = o.maxv(B, tf, lo, inv, "conservative")
+        full = tf[:, :, 3].max() - tf[:, :, 3].min()
+        assert ex <= r2 <= full
+
+
+def test_reduce_rgb_channels_constant_tf():
+    """P:250-256 (RGBa per bin after the division): with constant colour channels r = 0.1,
+    g = 0.2, b = 0.3 every vertex carries exactly those values (O8 is exact for constant
+    tables), so a channel-order mistake in the reduction's epilogue fails here."""
+    B, tf = _index_range_fixture()
+    U = o.update(B, tf, 5, P=1.0, eps=0.025, domain=[[0.0, 8.0]])
+    for m in range(2):
+        assert np.all(U.vertices[m]["r"] == f32(0.1))
+        assert np.all(U.vertices[m]["g"] == f32(0.2))
+        assert np.all(U.vertices[m]["b"] == f32(0.3))
+    # distinct ramps per channel: r = t, g = 1 - t, b = t/2 (exact at every t on N = 2
+    # tables with these knots up to one fp32 rounding); y uses alpha
+    tf2 = np.zeros((2, 2, 4), f32)
+    tf2[:, :, 0] = [0.0, 1.0]
+    tf2[:, :, 1] = [1.0, 0.0]
+    tf2[:, :, 2] = [0.0, 0.5]
+    tf2[:, :, 3] = [0.0, 1.0]
+    U = o.update(B, tf2, 5, P=1.0, eps=0.025, domain=[[0.0, 8.0]])
+    for m in range(2):
+        v = U.vertices[m]
+        mu = v["t_mean"].astype(np.float64)
+        assert np.all(v["r"] == v["t_mean"]) and np.all(v["y"] == v["t_mean"])
+        assert np.allclose(v["g"], 1.0 - mu, atol=1e-7) and np.allclose(v["b"], mu / 2, atol=1e-7)
