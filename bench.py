@@ -446,7 +446,7 @@ def run_native(args, rank, world, local):
     # range of the others (8 B) and the level; pass 2 (design D3) streams, per warp tile of
     # 128 cells, its q sum and running sum (16 B) and its M t-statistics (16 M B)
     tma = M <= 16
-    edit_cache = tma and M >= 3 and os.environ.get("DVL_EDIT_CACHE", "1") != "0"
+    edit_cache = tma and M >= 3
     bytes_cell = {"weights_scan_ms": 13 if edit_cache else 4 * M + 1,
                   "bin_reduce_ms": (16 * M + 16) / 128}
     dom = max(bytes_cell, key=lambda k: per_kernel[k])

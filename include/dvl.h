@@ -71,6 +71,11 @@ typedef void (*dvl_free_fn)(void *ptr, size_t bytes, void *cuda_stream, void *us
 #define DVL_FLAG_TIMING 1u   /* record CUDA events around every kernel (dvl_get_timings) */
 #define DVL_FLAG_GENERIC 2u  /* use the portable one-tile-per-CTA update kernels instead of
                                 the persistent TMA-pipelined ones (always used for M > 16) */
+/* Test / diagnostic flags: they select among kernels that return identical bits. */
+#define DVL_FLAG_NO_EDIT_CACHE 4u  /* every TF edit streams every member (no edit cache) */
+#define DVL_FLAG_PASS2_INLINE 8u   /* pass 2 folds its boundary warp tiles itself ... */
+#define DVL_FLAG_PASS2_LIST 16u    /* ... or lists them for the GPU-wide boundary kernel
+                                      (default: chosen from W, the tiles and the SM count) */
 
 typedef struct {
     int device;             /* CUDA device ordinal */
@@ -211,8 +216,10 @@ dvl_status dvl_get_polylines(dvl_ctx *ctx, uint32_t W, dvl_vertex *out, dvl_mem 
 /* ---- sharding: one context per GPU, each holding a contiguous range of the global curve
  * order.  Only two things cross shards per TF edit: the scan offset (the
  * sum of the earlier shards' fixed-point weights) and the per-pixel accumulators, which
- * are integers and merge exactly with a MAX and a SUM collective.  The caller runs the
- * collectives (e.g. torch.distributed over NCCL); the library never links NCCL. ---------- */
+ * are integers and merge exactly with a MAX and a SUM collective.  Either the context
+ * runs them itself on its own NCCL communicator (dvl_set_comm: libnccl.so.2 is loaded at
+ * run time with dlopen, so there is no link-time NCCL dependency), or the caller runs them
+ * between dvl_shard_reduce and dvl_shard_finish (e.g. torch.distributed over gloo). ------- */
 
 /* Hilbert bits of the whole dataset, used by the next dvl_build of this shard instead of
  * the shard's own extent (codes depend on b, so all shards must agree).  0 = own extent.

@@ -110,6 +110,7 @@ struct dvl_ctx {
   int launches = 0;
   int num_sms = 148;
   int acc_par = 0;                        // which lo / hi copy the next call uses
+  uint32_t acc_dirty[2] = {0, 0};         // per lo / hi copy: pixels [0, w) not yet restored
   bool volume = false;                    // dvl_set_level_scale: weights by cell volume
   // dvl_set_comm: the context's own NCCL communicator over the shards; dvl_get_polylines
   // then runs the sharded edit (both exchanges) itself
@@ -118,7 +119,8 @@ struct dvl_ctx {
   unsigned long long* d_totals = nullptr;   // [comm_ranks]
   int64_t* d_export = nullptr;              // the accumulator export, merged in place
   uint64_t export_cap = 0;
-  bool edit_cache = true;                 // DVL_EDIT_CACHE=0: every edit reads every member
+  bool edit_cache = true;                 // DVL_FLAG_NO_EDIT_CACHE: every edit reads every member
+  int pass2_mode = 0;                     // 0 auto, 1 boundary tiles inline, 2 listed (flags)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
   int stages_override = 0;
   int dbg = 0;                // experiment: pass-2 ring depth
@@ -284,6 +286,7 @@ UpdParams upd_params(dvl_ctx* ctx) {
   p.offset = 0;
   p.prod_sleep = ctx->prod_sleep;
   p.dbg = ctx->dbg;
+  p.pass2_mode = ctx->pass2_mode;
   p.cmin = d.cmin;
   p.cmax = d.cmax;
   p.cmember = -1;
@@ -499,6 +502,7 @@ void ensure_acc(dvl_ctx* ctx, uint32_t W) {
   dfree(ctx, ctx->d_bin_hi);
   ctx->acc = a;
   ctx->acc_par = 0;
+  ctx->acc_dirty[0] = ctx->acc_dirty[1] = 0;
   ctx->d_out = out;
   ctx->d_bin_lo = blo;
   ctx->d_bin_hi = bhi;
@@ -611,10 +615,14 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     }
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     // experiment knobs
+    ctx->edit_cache = !(init->flags & DVL_FLAG_NO_EDIT_CACHE);
+    ctx->pass2_mode = (init->flags & DVL_FLAG_PASS2_LIST) ? 2 : (init->flags & DVL_FLAG_PASS2_INLINE) ? 1 : 0;
+#ifdef DVL_PROF
+    // experiment knobs of the profiling build only
     if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
     if (const char* e = getenv("DVL_STAGES2")) ctx->stages_override = atoi(e);
     if (const char* e = getenv("DVL_DBG")) ctx->dbg = atoi(e);
-    if (const char* e = getenv("DVL_EDIT_CACHE")) ctx->edit_cache = atoi(e) != 0;
+#endif
     ctx->d_maxv = dalloc<float>(ctx, 1);
     ctx->d_qtot = dalloc<unsigned long long>(ctx, 1);
     ctx->d_ctr1 = dalloc<uint32_t>(ctx, 1);
@@ -1117,6 +1125,19 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     launch_epilogue(a, W, d.M, ctx->N, d.d_rgba, dst, ctx->d_bin_lo, ctx->d_bin_hi, ctx->d_err,
                     check ? herr_dev : nullptr, ctx->stream);
     CKLAUNCH();
+    // the epilogue restored the other copy over [0, W); if an earlier, wider call left
+    // pixels beyond W in it, restore those too, so the next call (which uses it) starts
+    // from the identity whatever its width
+    {
+      const int other = ctx->acc_par ^ 1;
+      if (ctx->acc_dirty[other] > W) {
+        const size_t tail = (size_t)(ctx->acc_dirty[other] - W) * sizeof(unsigned long long);
+        CK(cudaMemsetAsync(a.lo2 + W, 0xff, tail, ctx->stream));
+        CK(cudaMemsetAsync(a.hi2 + W, 0x00, tail, ctx->stream));
+      }
+      ctx->acc_dirty[other] = 0;
+      ctx->acc_dirty[ctx->acc_par] = W;
+    }
     ctx->acc_par ^= 1;   // this call's copy is restored by the next call's epilogue
     toc(ctx, PH_EPI);
     ctx->last_W = W;
@@ -1540,7 +1561,9 @@ dvl_status dvl_get_timings(dvl_ctx* ctx, dvl_timings* t) {
 
 }  // extern "C"
 
-// timing experiments: pass-2 phase clock sums (see update_tma.cu); not part of dvl.h
+#ifdef DVL_PROF
+// timing experiments of the profiling build: pass-2 phase clock sums (see update_tma.cu);
+// not part of dvl.h
 extern "C" __attribute__((visibility("default"))) int dvl_debug_stats(unsigned long long* out) {
   return dvl::debug_stats(out, true) == cudaSuccess ? 0 : 1;
 }
@@ -1550,3 +1573,4 @@ extern "C" __attribute__((visibility("default"))) int dvl_debug_bt(unsigned long
 extern "C" __attribute__((visibility("default"))) int dvl_debug_tl2(unsigned long long* out) {
   return dvl::debug_tl2(out) == cudaSuccess ? 0 : 1;
 }
+#endif

@@ -21,6 +21,9 @@ STATUS = {0: "DVL_OK", 1: "DVL_E_INVAL", 2: "DVL_E_STATE", 3: "DVL_E_RANGE", 4: 
           5: "DVL_E_DEGENERATE", 6: "DVL_E_NOMEM", 7: "DVL_E_CUDA", 8: "DVL_E_NCCL"}
 FLAG_TIMING = 1
 FLAG_GENERIC = 2
+FLAG_NO_EDIT_CACHE = 4
+FLAG_PASS2_INLINE = 8
+FLAG_PASS2_LIST = 16
 
 # every symbol include/dvl.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "dvl_build",
@@ -133,6 +136,44 @@ def _is_device(a) -> bool:
     return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
 
 
+def _need(cond: bool, msg: str):
+    """Argument validation in the binding: wrong dtypes / sizes would be misread by the C
+    library, which only sees pointers."""
+    if not cond:
+        raise ValueError(msg)
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def _torch_allocator(device: int):
+    """dvl_init's alloc / free callbacks backed by PyTorch's caching allocator (SURVEY 8(b):
+    "PyTorch only for device memory and streams").  None if torch / CUDA is unavailable."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return None
+    except Exception:
+        return None
+
+    def alloc(nbytes, stream, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(max(int(nbytes), 1), device=device,
+                                                      stream=int(stream or 0))
+        except Exception:
+            return None
+
+    def free(ptr, nbytes, stream, user):
+        try:
+            if ptr:
+                torch.cuda.caching_allocator_delete(ptr)
+        except Exception:
+            pass
+
+    return _ALLOC_FN(alloc), _FREE_FN(free)
+
+
 def hilbert_encode_host(xyz, bits: int) -> np.ndarray:
     """The library's table-driven Hilbert encoder evaluated on the host (no GPU)."""
     xyz = np.ascontiguousarray(np.asarray(xyz, dtype=np.uint32).reshape(-1, 3))
@@ -150,13 +191,26 @@ def hilbert_states() -> int:
 class Context:
     """One dvl_ctx: a dataset on one device plus its TFs, parameters and scratch."""
 
-    def __init__(self, device: int = 0, stream=None, timing: bool = False, generic: bool = False):
+    def __init__(self, device: int = 0, stream=None, timing: bool = False, generic: bool = False,
+                 torch_allocator: bool = True, edit_cache: bool = True, pass2: str | None = None):
+        """torch_allocator: device memory through PyTorch's caching allocator (dvl_init's
+        alloc / free callbacks); False: the library's own cudaMallocAsync pool.
+        edit_cache=False / pass2="inline"|"list": test flags selecting among kernels that
+        return identical bits (DVL_FLAG_NO_EDIT_CACHE, DVL_FLAG_PASS2_*)."""
         self._lib = load()
         init = _Init()
         init.device = device
+        self.device = device
         if stream is not None:
             init.cuda_stream = stream if isinstance(stream, int) else stream.cuda_stream
-        init.flags = (FLAG_TIMING if timing else 0) | (FLAG_GENERIC if generic else 0)
+        init.flags = (FLAG_TIMING if timing else 0) | (FLAG_GENERIC if generic else 0) \
+            | (0 if edit_cache else FLAG_NO_EDIT_CACHE) \
+            | {None: 0, "inline": FLAG_PASS2_INLINE, "list": FLAG_PASS2_LIST}[pass2]
+        self._alloc = _torch_allocator(device) if torch_allocator else None
+        if self._alloc is not None:
+            init.alloc = ctypes.cast(self._alloc[0], ctypes.c_void_p)
+            init.free = ctypes.cast(self._alloc[1], ctypes.c_void_p)
+        self._ext = None
         h = ctypes.c_void_p()
         st = self._lib.dvl_create(ctypes.byref(init), ctypes.byref(h))
         if st:
@@ -192,6 +246,25 @@ class Context:
     def stream(self) -> int:
         return int(self._lib.dvl_stream(self._h) or 0)
 
+    def _torch_stream(self):
+        import torch
+        if self._ext is None:
+            self._ext = torch.cuda.ExternalStream(self.stream, device=torch.device("cuda", self.device))
+        return self._ext
+
+    def _order_in(self, *tensors):
+        """Device inputs: the context stream waits for the caller's current stream (which
+        produced them, e.g. a .contiguous() copy) before the library reads them."""
+        import torch
+        for t in tensors:
+            _need(t.device.index == self.device, f"tensor on {t.device}, context on cuda:{self.device}")
+        self._torch_stream().wait_stream(torch.cuda.current_stream(self.device))
+
+    def _order_out(self):
+        """Device outputs: the caller's current stream waits for the context stream."""
+        import torch
+        torch.cuda.current_stream(self.device).wait_stream(self._torch_stream())
+
     # ------------------------------------------------------------------ the ABI
     def build(self, lower, level, scalars):
         """lower: (n,3) u32, level: (n,) u8, scalars: (M,n) f32 -- all numpy (host) or all
@@ -204,11 +277,20 @@ class Context:
             if scalars.ndim == 1:
                 scalars = scalars[None]
         else:
+            import torch
+            _need(_is_device(level) and _is_device(scalars), "all build inputs on the device, or all on the host")
+            _need(lower.dtype in (torch.int32, torch.uint32), "lower: int32/uint32 tensor")
+            _need(level.dtype == torch.uint8, "level: uint8 tensor")
+            _need(scalars.dtype == torch.float32, "scalars: float32 tensor")
             lower, level, scalars = lower.contiguous(), level.contiguous(), scalars.contiguous()
             if scalars.dim() == 1:
                 scalars = scalars[None]
+            self._order_in(lower, level, scalars)
         n = int(level.shape[0])
         M = int(scalars.shape[0])
+        _need(level.ndim == 1, "level: shape (n,)")
+        _need(int(np.prod(tuple(lower.shape))) == 3 * n, "lower: shape (n, 3)")
+        _need(tuple(scalars.shape) == (M, n), "scalars: shape (M, n)")
         ptrs = (ctypes.c_void_p * max(M, 1))(*[_ptr(scalars) + 4 * n * m for m in range(M)])
         st = self._lib.dvl_build(self._h, n, _ptr(lower), _ptr(level), M, ptrs,
                                  DEVICE if dev else HOST)
@@ -237,11 +319,18 @@ class Context:
     def get_polylines(self, W: int, out=None):
         """Returns an (M, W) structured numpy array (VERTEX_DTYPE); with ``out`` a torch
         CUDA tensor of >= M*W*32 bytes, writes there on the device and returns it."""
+        nbytes = self.M * int(W) * VERTEX_DTYPE.itemsize
         if out is not None and _is_device(out):
+            _need(out.is_contiguous() and out.numel() * out.element_size() >= nbytes,
+                  f"out: contiguous device tensor of >= {nbytes} bytes")
+            self._order_in(out)
             self._check(self._lib.dvl_get_polylines(self._h, W, _ptr(out), DEVICE),
                         "dvl_get_polylines")
+            self._order_out()
             return out
         res = np.empty((self.M, W), VERTEX_DTYPE) if out is None else out
+        _need(isinstance(res, np.ndarray) and res.flags.c_contiguous and res.nbytes >= nbytes,
+              f"out: contiguous numpy array of >= {nbytes} bytes")
         self._check(self._lib.dvl_get_polylines(self._h, W, _ptr(res), HOST), "dvl_get_polylines")
         return res
 
@@ -258,11 +347,14 @@ class Context:
             codes = torch.empty(self.n, dtype=torch.int64, device="cuda")
             ids = torch.empty(self.n, dtype=torch.int64, device="cuda")
             where = DEVICE
+            self._order_in(codes, ids)
         else:
             codes = np.empty(self.n, np.uint64)
             ids = np.empty(self.n, np.uint64)
             where = HOST
         self._check(self._lib.dvl_get_sorted(self._h, _ptr(codes), _ptr(ids), where), "dvl_get_sorted")
+        if device:
+            self._order_out()
         return codes, ids
 
     def get_sorted_data(self, device: bool = False):
@@ -273,12 +365,15 @@ class Context:
             lv = torch.empty(self.n, dtype=torch.uint8, device="cuda")
             sc = torch.empty((self.M, self.n), dtype=torch.float32, device="cuda")
             where = DEVICE
+            self._order_in(lv, sc)
         else:
             lv = np.empty(self.n, np.uint8)
             sc = np.empty((self.M, self.n), np.float32)
             where = HOST
         self._check(self._lib.dvl_get_sorted_data(self._h, _ptr(lv), _ptr(sc), where),
                     "dvl_get_sorted_data")
+        if device:
+            self._order_out()
         return lv, sc
 
     def get_prefix(self) -> np.ndarray:
@@ -300,10 +395,14 @@ class Context:
         tensor in -> torch CUDA int64 out."""
         if _is_device(xyz):
             import torch
+            _need(xyz.dtype in (torch.int32, torch.uint32) and xyz.numel() % 3 == 0,
+                  "xyz: int32/uint32 tensor of shape (n, 3)")
             xyz = xyz.contiguous()
             out = torch.empty(xyz.numel() // 3, dtype=torch.int64, device=xyz.device)
+            self._order_in(xyz, out)
             self._check(self._lib.dvl_locate(self._h, out.numel(), _ptr(xyz), _ptr(out), DEVICE),
                         "dvl_locate")
+            self._order_out()
             return out
         xyz = np.ascontiguousarray(np.asarray(xyz, dtype=np.uint32).reshape(-1, 3))
         out = np.empty(len(xyz), np.int64)
@@ -339,20 +438,30 @@ class Context:
 
     def shard_total(self, dst):
         """Copy this shard's weight total into dst (a torch CUDA int64 tensor element)."""
+        self._order_in(dst)
         self._check(self._lib.dvl_shard_total(self._h, _ptr(dst)), "dvl_shard_total")
+        self._order_out()
 
     def shard_export_words(self, W: int) -> int:
         return int(self._lib.dvl_shard_export_words(self._h, W))
 
     def shard_reduce(self, W: int, totals, shard: int, export):
         """totals: CUDA int64 tensor [nshards]; export: CUDA int64 tensor of export words."""
+        import torch
+        _need(totals.dtype == torch.int64 and export.dtype == torch.int64
+              and export.numel() >= self.shard_export_words(W), "totals / export: int64 tensors")
+        self._order_in(totals, export)
         self._check(self._lib.dvl_shard_reduce(self._h, W, _ptr(totals), int(totals.numel()),
                                                shard, _ptr(export)), "dvl_shard_reduce")
+        self._order_out()
 
     def shard_finish(self, W: int, merged, out=None):
+        self._order_in(merged)
         if out is not None and _is_device(out):
+            _need(out.numel() * out.element_size() >= self.M * int(W) * VERTEX_DTYPE.itemsize, "out too small")
             self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(out), DEVICE),
                         "dvl_shard_finish")
+            self._order_out()
             return out
         res = np.empty((self.M, W), VERTEX_DTYPE) if out is None else out
         self._check(self._lib.dvl_shard_finish(self._h, W, _ptr(merged), _ptr(res), HOST),

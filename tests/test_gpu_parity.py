@@ -259,17 +259,12 @@ def test_edit_cache_sequences(dvl, M):
     range of the others): edit sequences that switch members, change a domain, reset the
     TFs and change P / eps in between, each checked against the oracle, and against a
     context with the cache disabled (bit for bit)."""
-    import os
     lower, level = octree(32, 3, 60 + M)
     scal = scalars(len(level), M, 61 + M, nan_frac=0.01)
     B = o.build(lower, level, scal)
     ctx = make_ctx(dvl)
     ctx.build(lower, level, scal)
-    os.environ["DVL_EDIT_CACHE"] = "0"
-    try:
-        ref_ctx = make_ctx(dvl)
-    finally:
-        del os.environ["DVL_EDIT_CACHE"]
+    ref_ctx = dvl.Context(device=0, edit_cache=False)
     ref_ctx.build(lower, level, scal)
     tfs = tfs_for(M, 256, 62)
     for c in (ctx, ref_ctx):
@@ -361,7 +356,8 @@ def test_device_buffers(dvl):
         ctx.update_tf(m, tfs[m])
     out = torch.empty(4 * 1024 * 8, dtype=torch.int32, device="cuda")
     ctx.get_polylines(1024, out=out)
-    torch.cuda.synchronize()
+    # no explicit synchronize: the binding orders the caller's current stream after the
+    # context stream, so reading 'out' on the current stream sees the epilogue's writes
     got = out.cpu().numpy().view(dvl.VERTEX_DTYPE).reshape(4, 1024)
     assert np.array_equal(got["count"], U.vertices["count"])
     assert np.array_equal(got["t_min"], U.vertices["t_min"])
@@ -412,3 +408,74 @@ def test_negative_zero_and_domain_edges(dvl, path):
     scal[2, 1::7] = -1.0
     dom = np.array([[0.0, 2.0], [0.0, 1.5], [0.0, 2.0]], f32)
     parity(dvl, lower, level, scal, tfs_for(3, 256, 73), 64, domain=dom, generic=path == "generic")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_width_shrinks_then_grows(dvl, path):
+    """W = 1024, 512, 700, 2048, 3 on one context, with and without TF edits in between:
+    the two alternating lo / hi copies must not carry first / last cells of an earlier,
+    wider call into a later one."""
+    lower, level = octree(32, 3, 81)
+    scal = scalars(len(level), 4, 82)
+    B = o.build(lower, level, scal)
+    ctx = make_ctx(dvl, path == "generic")
+    ctx.build(lower, level, scal)
+    tfs = tfs_for(4, 256, 83)
+    for m in range(4):
+        ctx.update_tf(m, tfs[m])
+    for k, W in enumerate((1024, 512, 700, 2048, 3, 1500, 1499, 4096)):
+        if k % 2:
+            tfs[0] = synth.tf_edit(4, k)
+            ctx.update_tf(0, tfs[0])
+        a = ctx.get_polylines(W)
+        U = o.update(B, tfs, W)
+        g = dict(out=a, info=ctx.info(), Q=ctx.get_prefix(), ranges=ctx.get_bin_ranges(W))
+        check_update(U, B, tfs, g, W)
+    ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["conservative", "per_entry"])
+@pytest.mark.parametrize("path", PATHS)
+def test_maxv_data_index_range(dvl, mode, path):
+    """the max(V_h) approximation only visits the TF entries [i, j] that the data
+    reach.  Domains twice as wide as the data put [i, j] strictly inside [0, N-1], and the
+    TFs' alpha extremes outside it: the device's maxV must equal the oracle's and differ
+    from the whole-table value."""
+    lower, level = octree(32, 2, 24)
+    n = len(level)
+    rng = np.random.default_rng(25)
+    M, N = 3, 64
+    scal = np.stack([(2.0 + m * 0.5 + rng.random(n)).astype(f32) for m in range(M)])
+    # member ranges [2,3], [2.5,3.5], [3,4] on the domain [0, 8] -> [i, j] ~ [15, 32] of 63
+    tfs = tfs_for(M, N, 26)
+    tfs[:, :8, 3] = 0.0
+    tfs[:, -8:, 3] = 1.0
+    tfs[:, 8:-8, 3] = np.clip(tfs[:, 8:-8, 3], 0.1, 0.9)
+    B, U, g = parity(dvl, lower, level, scal, tfs, 700, mode=mode, domain=[[0.0, 8.0]],
+                     generic=path == "generic")
+    lo, _, inv = o.domains(B, [[0.0, 8.0]])
+    ij = [o.index_range(float(B.vmin[m]), float(B.vmax[m]), float(lo[m]), float(inv[m]), N) for m in range(M)]
+    assert min(i for i, _ in ij) > 8 and max(j for _, j in ij) < N - 9
+    full = float(tfs[:, :, 3].max() - tfs[:, :, 3].min()) if mode == "conservative" else \
+        float((tfs[:, :, 3].max(0) - tfs[:, :, 3].min(0)).max())
+    assert g["info"]["maxV"] == U.maxV and U.maxV < full
+
+
+def test_binding_validates_device_arguments(dvl):
+    """The binding rejects device tensors of the wrong dtype / size instead of letting the
+    C library misread them."""
+    import torch
+    lower, level = octree(16, 2, 62)
+    scal = scalars(len(level), 2, 63)
+    ctx = make_ctx(dvl)
+    with pytest.raises(ValueError):
+        ctx.build(torch.from_numpy(lower.astype(np.int64)).cuda(), torch.from_numpy(level).cuda(),
+                  torch.from_numpy(scal).cuda())
+    with pytest.raises(ValueError):
+        ctx.build(torch.from_numpy(lower.astype(np.int32)).cuda(), torch.from_numpy(level).cuda(),
+                  torch.from_numpy(scal.astype(np.float64)).cuda())
+    ctx.build(torch.from_numpy(lower.astype(np.int32)).cuda(), torch.from_numpy(level).cuda(),
+              torch.from_numpy(scal).cuda())
+    with pytest.raises(ValueError):
+        ctx.get_polylines(64, out=torch.empty(2 * 64 * 8 - 1, dtype=torch.int32, device="cuda"))
+    ctx.close()
