@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded path (collectives) even at N=1")
+    ap.add_argument("--also", default=None,
+                    help="comma-separated extra configs measured after the main one (N=1, own "
+                         "subprocess) and reported under 'also'; default C3 with C2; 'none'")
     return ap.parse_args()
 
 
@@ -63,15 +66,31 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+def load_traffic(config: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` on `config`, from
+    the committed ncu --set full captures (profiles/ncu_dram_per_launch.json, keyed by
+    config), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(kernel)
+        return d.get(config, {}).get(kernel)
     except Exception:
         return None
+
+
+def host_cpu():
+    """nproc and the CPU model of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 class ClockSampler:
@@ -129,9 +148,25 @@ class ClockSampler:
 
 
 def workload(name):
+    """Host (numpy) inputs of a config -- the reference arm and the CPU baseline."""
     import synth
     c = synth.make_config(name)
     return c
+
+
+def device_workload(name, dev, seed):
+    """Device-resident inputs of a config: the ensemble configs are generated in HBM
+    (synth/device.py, the same recipe and bits as synth/); the multi-field C3 on the host."""
+    import torch
+    import synth
+    if synth.CONFIGS[name][7]:   # multi-field
+        c = synth.make_config(name, seed=seed)
+        c["lower"] = torch.from_numpy(c["lower"].view(np.int32)).to(dev)
+        c["level"] = torch.from_numpy(c["level"]).to(dev)
+        c["scal"] = torch.from_numpy(c["scal"]).to(dev)
+        return c
+    from synth import device as sd
+    return sd.make_config(name, device=dev, seed=seed)
 
 
 def tf_sequence(cfg_name, count, N, M):
@@ -213,7 +248,8 @@ def cpu_baseline(c, edits_base, W, budget_s=20.0):
     from oracle import oracle as o
     n_full = len(c["level"])
     t0 = time.perf_counter()
-    B = o.build(c["lower"], c["level"], c["scal"])
+    host = lambda a: a if isinstance(a, np.ndarray) else a.cpu().numpy()
+    B = o.build(host(c["lower"]).view(np.uint32), host(c["level"]), host(c["scal"]))
     t_build = time.perf_counter() - t0
     tfs = np.stack(edits_base)
     times = []
@@ -225,7 +261,8 @@ def cpu_baseline(c, edits_base, W, budget_s=20.0):
     sec = statistics.median(times)
     return {"value": n_full / sec / 1e9, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
             "sample": f"{len(times)} full TF-update passes of {args_cfg_name} ({n_full} cells), "
-                      f"median; oracle build {t_build:.2f} s"}
+                      f"median; oracle build {t_build:.2f} s",
+            **host_cpu(), "threads_used": 1}
 
 
 args_cfg_name = "C2"
@@ -248,30 +285,28 @@ def run_native(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import synth
+    dev = torch.device("cuda", local)
     # sharded (N > 1): weak scaling over a 2x larger logical grid whose first `world`
     # octants in curve order each hold one rank's config-sized piece -- every rank owns one
     # contiguous range of the global Hilbert order (codes with one more bit)
-    c = synth.make_config(args.config, seed=synth.CELL_SEED + (rank if sharded else 0))
-    n = len(c["level"])
+    c = device_workload(args.config, dev, synth.CELL_SEED + (rank if sharded else 0))
+    n = int(c["level"].shape[0])
     M, W, N = c["M"], c["W"], 256
     base, edits = tf_sequence(args.config, args.warmup + args.steps, N, M)
     gbits = 0
+    lower_d, level_d, scal_d = c["lower"], c["level"], c["scal"]
     if sharded:
         b0 = int(np.ceil(np.log2(c["E"])))
         gbits = b0 + 1
         half = np.uint32(1 << b0)
         corners = np.array([[x, y, z] for x in (0, 1) for y in (0, 1) for z in (0, 1)], np.uint32) * half
         order = np.argsort(dvl.hilbert_encode_host(corners, gbits))
-        c["lower"] = (c["lower"] + corners[order[rank]]).astype(np.uint32)
+        lower_d = lower_d + torch.from_numpy(corners[order[rank]].astype(np.int32)).to(dev)[None, :]
 
     stream = torch.cuda.Stream()
     ctx = dvl.Context(device=local, stream=stream, timing=True)
     if gbits:
         ctx.set_global_bits(gbits)
-    dev = torch.device("cuda", local)
-    lower_d = torch.from_numpy(c["lower"].view(np.int32)).to(dev)
-    level_d = torch.from_numpy(c["level"]).to(dev)
-    scal_d = torch.from_numpy(c["scal"]).to(dev)
     n_global = n * world
     if sharded:
         # the build's input is a round-robin slice of the global generator order (untimed
@@ -454,7 +489,7 @@ def run_native(args, rank, world, local):
     achieved = alg_bytes / (per_kernel[dom] / 1e3) / 1e9
     kname = {"weights_scan_ms": "weights_reduce_tma" if tma else "weights_scan_kernel",
              "bin_reduce_ms": "agg_reduce" if tma else "bin_reduce_kernel"}[dom]
-    traffic = load_traffic(kname)
+    traffic = load_traffic(args.config, kname)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
@@ -469,6 +504,22 @@ def run_native(args, rank, world, local):
             cpu = cpu_baseline(c, base, W)
         except Exception as ex:  # pragma: no cover
             cpu = {"error": str(ex)}
+    del c, lower_d, level_d, scal_d
+    ctx.close()
+    torch.cuda.empty_cache()
+    also = {}
+    extra = args.also if args.also is not None else ("C3" if args.config == "C2" else "none")
+    if world == 1 and extra != "none":
+        import subprocess
+        for cfg in extra.split(","):
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--config", cfg, "--steps",
+                                str(args.steps), "--warmup", str(args.warmup), "--no-cpu-baseline",
+                                "--also", "none", "--build-reps", str(args.build_reps)],
+                               capture_output=True, text=True)
+            try:
+                also[cfg] = json.loads(r.stdout.strip().splitlines()[-1])
+            except Exception:
+                also[cfg] = {"error": (r.stderr or r.stdout)[-400:]}
     bphase = {k: statistics.median([p[k] for p in phase]) for k in
               ("ingest_ms", "encode_ms", "sort_ms", "gather_ms")}
     emit({
@@ -495,6 +546,7 @@ def run_native(args, rank, world, local):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches,
+        **({"also": also} if also else {}),
     })
     if dist:
         dist.destroy_process_group()

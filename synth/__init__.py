@@ -43,10 +43,12 @@ def _point_key(ix, iy, iz):
 
 
 # ---------------------------------------------------------------------------- cells
-def uniform_cells(E: int):
-    """A uniform E^3 grid of level-0 cells, row-major (x fastest)."""
-    r = np.arange(E, dtype=np.uint32)
-    z, y, x = np.meshgrid(r, r, r, indexing="ij")
+def uniform_cells(E: int, box=None):
+    """A uniform E^3 grid of level-0 cells, row-major (x fastest); box = (gx, gy, gz) for a
+    gx x gy x gz block instead."""
+    gx, gy, gz = box if box is not None else (E, E, E)
+    z, y, x = np.meshgrid(np.arange(gz, dtype=np.uint32), np.arange(gy, dtype=np.uint32),
+                          np.arange(gx, dtype=np.uint32), indexing="ij")
     lower = np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1).astype(np.uint32)
     return np.ascontiguousarray(lower), np.zeros(len(lower), np.uint8)
 
@@ -102,13 +104,15 @@ class BlobField:
         return out
 
 
-def amr_cells(E: int, Lc: int, rho, seed: int = CELL_SEED, field: BlobField | None = None):
+def amr_cells(E: int, Lc: int, rho, seed: int = CELL_SEED, field: BlobField | None = None,
+              box=None):
     """Nested AMR: coarse level-Lc grid (row-major), then at each level refine the fraction
     rho[i] of the current finest cells with the largest field value + noise (refined
-    regions cluster around blob centres like real AMR), children in Morton order."""
+    regions cluster around blob centres like real AMR), children in Morton order.
+    box = (gx, gy, gz): a slab of coarse blocks instead of the whole (E >> Lc)^3 grid."""
     field = field or BlobField(seed)
     G = E >> Lc
-    lower, level = uniform_cells(G)
+    lower, level = uniform_cells(G, box)
     lower = lower << np.uint32(Lc)
     level = np.full(len(lower), Lc, np.uint8)
     for i, L in enumerate(range(Lc, 0, -1)):
@@ -216,17 +220,18 @@ CONFIGS = {
 }
 
 
-def make_config(name: str, seed: int = CELL_SEED, scale_E: int | None = None):
+def make_config(name: str, seed: int = CELL_SEED, scale_E: int | None = None, box=None):
     """Returns dict(lower, level, scal, W, M, E, domain) for a named config.  scale_E
-    shrinks the logical grid (same recipe) for quick tests."""
+    shrinks the logical grid (same recipe) for quick tests; box = (gx, gy, gz) keeps the
+    grid (so the Hilbert bits b) but generates only a slab of its coarse blocks."""
     kind, E, Lc, rho, M, W, dom, multi = CONFIGS[name]
     if scale_E is not None:
         E = scale_E
     field = BlobField(seed)
     if kind == "uniform":
-        lower, level = uniform_cells(E)
+        lower, level = uniform_cells(E, box)
     else:
-        lower, level = amr_cells(E, Lc, rho, seed, field)
+        lower, level = amr_cells(E, Lc, rho, seed, field, box)
     scal = member_scalars(lower, level, E, M, seed, MEMBER_SEED, field, multifield=multi)
     if dom == "shared":
         fin = scal[np.isfinite(scal)]

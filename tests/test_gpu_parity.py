@@ -375,24 +375,7 @@ def test_full_size_config(dvl, name, path):
            generic=path == "generic")
 
 
-@pytest.mark.parametrize("path", PATHS)
-def test_c3_recipe_several_pass2_waves(dvl, path):
-    """BASELINE configs[2]'s recipe (5 levels, 8 fields, per-member domains, W = 4096) on a
-    1024^3 grid (~13 M cells): more pass-1 tiles than pass 2 keeps resident in one wave, so
-    pass 2 lists its boundary tiles for bin_boundary (the launch configuration C3 runs in)."""
-    if "C3s" not in _CACHE:
-        c = synth.make_config("C3", scale_E=1024)
-        tfs = np.stack([synth.tf_edit(3, 0, member=m) for m in range(c["M"])])
-        B = o.build(c["lower"], c["level"], c["scal"])
-        _CACHE["C3s"] = (c, tfs, B, o.update(B, tfs, c["W"]))
-    c, tfs, B, U = _CACHE["C3s"]
-    assert c["lower"].shape[0] > 148 * 3 * 8 * 16 * 128
-    g = run_gpu(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], generic=path == "generic")
-    check_build(B, g)
-    check_update(U, B, tfs, g, c["W"])
 
-
-_CACHE = {}
 
 
 @pytest.mark.parametrize("path", PATHS)
