@@ -76,6 +76,8 @@ typedef void (*dvl_free_fn)(void *ptr, size_t bytes, void *cuda_stream, void *us
 #define DVL_FLAG_PASS2_INLINE 8u   /* pass 2 folds its boundary warp tiles itself ... */
 #define DVL_FLAG_PASS2_LIST 16u    /* ... or lists them for the GPU-wide boundary kernel
                                       (default: chosen from W, the tiles and the SM count) */
+#define DVL_FLAG_LSD_SORT 32u      /* build with the onesweep LSD radix sort even where the
+                                      bucket sort applies (3b <= 36) */
 
 typedef struct {
     int device;             /* CUDA device ordinal */

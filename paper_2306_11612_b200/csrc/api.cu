@@ -734,7 +734,8 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     tmp.push_back(d_ing);
     CK(cudaMemcpyAsync(d_ing, &h_ing, sizeof h_ing, cudaMemcpyHostToDevice, st));
     int grid = (int)std::min<int64_t>((nn + kBlock - 1) / kBlock, 148 * 8);
-    launch_ingest(d_lower, d_level, d_ptrs, nn, M, d_ing, grid, st);
+    // geometry only: the member ranges are folded into the gather (B3)
+    launch_ingest_geom(d_lower, d_level, nn, d_ing, ctx->num_sms, st);
     CKLAUNCH();
     toc(ctx, PH_INGEST);
     CK(cudaMemcpyAsync(&h_ing, d_ing, sizeof h_ing, cudaMemcpyDeviceToHost, st));
@@ -759,86 +760,123 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
     const int64_t T = (int64_t)kBlock * d.items;
     d.tiles = (int)((nn + T - 1) / T);
     d.n_pad = (int64_t)d.tiles * T;
-    d.vmin.resize(M);
-    d.vmax.resize(M);
-    for (int m = 0; m < M; ++m) {
-      d.vmin[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmin[m]) : 0.0f;
-      d.vmax[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmax[m]) : 0.0f;
-    }
-
-    // ---- B1: Hilbert encode + digit histograms
+    // ---- B1: Hilbert encode (+ bucket counts or digit histograms)
     const int kb = d.key_bytes;
     void* kA = dmalloc(ctx, (size_t)kb * nn);
     void* kB = dmalloc(ctx, (size_t)kb * nn);
     uint32_t* iA = dalloc<uint32_t>(ctx, nn);
     uint32_t* iB = dalloc<uint32_t>(ctx, nn);
-    uint32_t* hist = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
-    uint32_t* base = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
-    const int64_t stiles = (nn + kSortTile - 1) / kSortTile;
-    uint32_t* status = dalloc<uint32_t>(ctx, (size_t)d.passes * stiles * 256);
-    uint32_t* ctrs = dalloc<uint32_t>(ctx, d.passes);
-    tmp.push_back(hist);
-    tmp.push_back(base);
-    tmp.push_back(status);
-    tmp.push_back(ctrs);
-    CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * d.passes * 256, st));
-    CK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * d.passes * stiles * 256, st));
-    CK(cudaMemsetAsync(ctrs, 0, sizeof(uint32_t) * d.passes, st));
-    tic(ctx, PH_ENCODE);
-    launch_encode_hist(d_lower, d_level, nn, d.b, kb, d.passes, ctx->d_t1, ctx->d_t2,
-                       ctx->nstates, kA, iA, hist, grid, st);
-    CKLAUNCH();
-    toc(ctx, PH_ENCODE);
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
+    const bool bucket = 3 * d.b <= 36 && !(ctx->flags & DVL_FLAG_LSD_SORT);
+    if (bucket) {
+      // B1 + B2 as the two-pass bucket sort of distinct codes (bsort.cu)
+      int lb = 0;
+      const int64_t nb = bucket_count(d.b, &lb);
+      const int64_t nblk = (nb + 4095) / 4096;
+      uint32_t* bcnt = dalloc<uint32_t>(ctx, (size_t)nb);
+      uint32_t* bstart = dalloc<uint32_t>(ctx, (size_t)nb + 1);
+      uint16_t* slot = dalloc<uint16_t>(ctx, (size_t)nn);
+      uint32_t* bsum = dalloc<uint32_t>(ctx, (size_t)nblk + 1);
+      uint32_t* work = dalloc<uint32_t>(ctx, 1);
+      tmp.push_back(bcnt);
+      tmp.push_back(bstart);
+      tmp.push_back(slot);
+      tmp.push_back(bsum);
+      tmp.push_back(work);
+      CK(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * nb, st));
+      CK(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));
+      tic(ctx, PH_ENCODE);
+      launch_encode_bucket(d_lower, d_level, nn, d.b, lb, kb, ctx->d_t1, ctx->d_t2, ctx->nstates,
+                           kA, slot, bcnt, ctx->num_sms, st);
+      CKLAUNCH();
+      toc(ctx, PH_ENCODE);
+      tic(ctx, PH_SORT);
+      launch_bucket_scan(bcnt, nb, lb, bsum, bstart, (uint32_t)nn, ctx->d_err, st);
+      CKLAUNCH();
+      launch_bucket_sort(kA, slot, kb, nn, lb, nb, bstart, kB, iB, kA, iA, work, ctx->d_err,
+                         ctx->num_sms, st);
+      CKLAUNCH();
+      toc(ctx, PH_SORT);
+      ctx->sort_passes = 2;
+      d.keys = kA;
+      d.perm = iA;
+      tmp.push_back(kB);
+      tmp.push_back(iB);
+    } else {
+      uint32_t* hist = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
+      uint32_t* base = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
+      const int64_t stiles = (nn + kSortTile - 1) / kSortTile;
+      uint32_t* status = dalloc<uint32_t>(ctx, (size_t)d.passes * stiles * 256);
+      uint32_t* ctrs = dalloc<uint32_t>(ctx, d.passes);
+      tmp.push_back(hist);
+      tmp.push_back(base);
+      tmp.push_back(status);
+      tmp.push_back(ctrs);
+      CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * d.passes * 256, st));
+      CK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * d.passes * stiles * 256, st));
+      CK(cudaMemsetAsync(ctrs, 0, sizeof(uint32_t) * d.passes, st));
+      tic(ctx, PH_ENCODE);
+      launch_encode_hist(d_lower, d_level, nn, d.b, kb, d.passes, ctx->d_t1, ctx->d_t2,
+                         ctx->nstates, kA, iA, hist, grid, st);
+      CKLAUNCH();
+      toc(ctx, PH_ENCODE);
 
-    // ---- B2: onesweep passes (a pass whose digit is constant is the identity: skipped)
-    tic(ctx, PH_SORT);
-    launch_hist_scan(hist, base, d.passes, st);
-    CKLAUNCH();
-    std::vector<uint32_t> h_hist((size_t)d.passes * 256);
-    CK(cudaMemcpyAsync(h_hist.data(), hist, 4 * h_hist.size(), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    void* kin = kA;
-    void* kout = kB;
-    uint32_t* vin = iA;
-    uint32_t* vout = iB;
-    int done = 0;
-    for (int p = 0; p < d.passes; ++p) {
-      uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
-      if ((int64_t)mx == nn) continue;
-      // the first pass generates the ids (iota) instead of reading them
-      launch_onesweep(kin, done == 0 ? nullptr : vin, kout, vout, nn, kb, 8 * p, base + p * 256,
-                      status + (size_t)p * stiles * 256, ctrs + p, st);
+      // ---- B2: onesweep passes (a pass whose digit is constant is the identity: skipped)
+      tic(ctx, PH_SORT);
+      launch_hist_scan(hist, base, d.passes, st);
       CKLAUNCH();
-      std::swap(kin, kout);
-      std::swap(vin, vout);
-      ++done;
+      std::vector<uint32_t> h_hist((size_t)d.passes * 256);
+      CK(cudaMemcpyAsync(h_hist.data(), hist, 4 * h_hist.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      void* kin = kA;
+      void* kout = kB;
+      uint32_t* vin = iA;
+      uint32_t* vout = iB;
+      int done = 0;
+      for (int p = 0; p < d.passes; ++p) {
+        uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
+        if ((int64_t)mx == nn) continue;
+        // the first pass generates the ids (iota) instead of reading them
+        launch_onesweep(kin, done == 0 ? nullptr : vin, kout, vout, nn, kb, 8 * p, base + p * 256,
+                        status + (size_t)p * stiles * 256, ctrs + p, st);
+        CKLAUNCH();
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+        ++done;
+      }
+      if (done == 0) {   // every digit constant (n == 1): the identity permutation
+        launch_iota(vin, nn, st);
+        CKLAUNCH();
+      }
+      ctx->sort_passes = done;
+      toc(ctx, PH_SORT);
+      d.keys = kin;
+      d.perm = vin;
+      tmp.push_back(kout);
+      tmp.push_back(vout);
     }
-    if (done == 0) {   // every digit constant (n == 1): the identity permutation
-      launch_iota(vin, nn, st);
-      CKLAUNCH();
-    }
-    ctx->sort_passes = done;
-    toc(ctx, PH_SORT);
-    d.keys = kin;
-    d.perm = vin;
-    tmp.push_back(kout);
-    tmp.push_back(vout);
 
     // ---- B3: permute into curve order + overlap validation
     d.level_s = dalloc<uint8_t>(ctx, d.n_pad);
     d.scal_s = dalloc<float>(ctx, (size_t)M * d.n_pad);
     CK(cudaMemsetAsync(d.level_s, 0, d.n_pad, st));
     CK(cudaMemsetAsync(d.scal_s, 0, sizeof(float) * M * d.n_pad, st));
-    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
     tic(ctx, PH_GATHER);
-    launch_gather_validate(d.keys, kb, d.perm, d_level, d_ptrs, nn, M, d.n_pad, d.level_s,
-                           d.scal_s, ctx->d_err, grid, st);
+    launch_gather_validate4(d.keys, kb, d.perm, d_level, d_ptrs, nn, M, d.n_pad, d.level_s,
+                            d.scal_s, ctx->d_err, d_ing, ctx->num_sms, st);
     CKLAUNCH();
     toc(ctx, PH_GATHER);
     uint32_t herr = 0;
     CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_ing, d_ing, sizeof h_ing, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (herr & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
+    d.vmin.resize(M);
+    d.vmax.resize(M);
+    for (int m = 0; m < M; ++m) {
+      d.vmin[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmin[m]) : 0.0f;
+      d.vmax[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmax[m]) : 0.0f;
+    }
 
     // ---- per-dataset update state
     d.d_vmin = dalloc<float>(ctx, M);

@@ -24,6 +24,18 @@ void launch_encode_hist(const uint32_t* lower, const uint8_t* level, int64_t n, 
                         int nstates, void* keys, uint32_t* ids, uint32_t* hist, int grid,
                         cudaStream_t st);
 
+void launch_encode_bucket(const uint32_t* lower, const uint8_t* level, int64_t n, int b, int lb,
+                          int key_bytes, const uint16_t* d_t1, const uint16_t* d_t2, int nstates,
+                          void* keys, uint16_t* slot, uint32_t* count, int num_sms, cudaStream_t st);
+
+// bsort.cu (3b <= 36)
+int64_t bucket_count(int b, int* lb);
+void launch_bucket_scan(const uint32_t* cnt, int64_t nb, int lb, uint32_t* bsum, uint32_t* start,
+                        uint32_t total, uint32_t* err, cudaStream_t st);
+void launch_bucket_sort(const void* keys, const uint16_t* slot, int key_bytes, int64_t n, int lb,
+                        int64_t nb, const uint32_t* start, void* kA, uint32_t* vA, void* kB,
+                        uint32_t* vB, uint32_t* work, uint32_t* err, int num_sms, cudaStream_t st);
+
 // sort.cu
 cudaError_t prepare_onesweep();
 void launch_hist_scan(const uint32_t* hist, uint32_t* base, int passes, cudaStream_t st);
@@ -40,12 +52,12 @@ struct IngestOut {                 // device-side results of the ingest reductio
   uint32_t vmax[64];
   uint32_t any[64];               // 1 if the member has a finite value
 };
-void launch_ingest(const uint32_t* lower, const uint8_t* level, const float* const* scal,
-                   int64_t n, int M, IngestOut* out, int grid, cudaStream_t st);
-void launch_gather_validate(const void* keys, int key_bytes, const uint32_t* perm,
-                            const uint8_t* level_in, const float* const* scal_in, int64_t n,
-                            int M, int64_t n_pad, uint8_t* level_s, float* scal_s,
-                            uint32_t* err, int grid, cudaStream_t st);
+void launch_ingest_geom(const uint32_t* lower, const uint8_t* level, int64_t n, IngestOut* out,
+                        int num_sms, cudaStream_t st);
+void launch_gather_validate4(const void* keys, int key_bytes, const uint32_t* perm,
+                             const uint8_t* level_in, const float* const* scal_in, int64_t n,
+                             int M, int64_t n_pad, uint8_t* level_s, float* scal_s, uint32_t* err,
+                             IngestOut* ranges, int num_sms, cudaStream_t st);
 void launch_widen(const void* keys, int key_bytes, const uint32_t* perm, int64_t n,
                   uint64_t* codes_out, uint64_t* ids_out, cudaStream_t st);
 float ordered_to_float(uint32_t u);

@@ -151,6 +151,161 @@ __device__ __forceinline__ int two_levels(uint32_t x, uint32_t y, uint32_t z, in
                ((yb & 1) << 1) | (zb & 1));
 }
 
+// the code with the two-level table stored in coordinate-major index order
+// (x_j x_{j-1} y_j y_{j-1} z_j z_{j-1}): each step takes 2 bits of x, y and z directly,
+// with no bit interleaving; the code accumulates in K (32-bit for 3b <= 32)
+template <typename K>
+__device__ __forceinline__ K hilbert_code_cm(uint32_t x, uint32_t y, uint32_t z, int b,
+                                             const uint16_t* s_t1, const uint16_t* s_t2p) {
+  uint32_t s = 0;
+  K code = 0;
+  int j = b - 1;
+  if (b & 1) {
+    const uint32_t oct = (((x >> j) & 1u) << 2) | (((y >> j) & 1u) << 1) | ((z >> j) & 1u);
+    const uint32_t e = s_t1[oct];
+    code = (K)(e & 7u);
+    s = e >> 3;
+    --j;
+  }
+  for (; j >= 1; j -= 2) {
+    const uint32_t idx = (((x >> (j - 1)) & 3u) << 4) | (((y >> (j - 1)) & 3u) << 2) | ((z >> (j - 1)) & 3u);
+    const uint32_t e = s_t2p[s * 64 + idx];
+    code = (code << 6) | (K)(e & 63u);
+    s = e >> 6;
+  }
+  return code;
+}
+
+// B1 for the bucket sort (3b <= 36, see bsort.cu): four cells per thread with 16-byte
+// loads of the AoS corners (3 x uint4 = 4 cells) and one 4-byte load of their levels, the
+// four codes stored with one (u32) or two (u64) 16-byte stores, and the bucket counts
+// (bucket = code >> lb, an aligned run of 2^lb codes) taken with one returning global
+// atomic per bucket per warp (lanes grouped by __match_any_sync: consecutive input cells
+// mostly share a bucket).  The value an atomic returns gives each cell a slot inside its
+// bucket (any order: the rank pass orders the bucket), stored as a u16 next to the code,
+// so the scatter pass needs no atomics.
+template <typename K, bool VEC>
+__global__ void __launch_bounds__(kBlock)
+encode_bucket_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restrict__ level,
+                     int64_t n, int b, int lb, const uint16_t* __restrict__ t1g,
+                     const uint16_t* __restrict__ t2g, int nstates, K* __restrict__ keys,
+                     uint16_t* __restrict__ slot, uint32_t* __restrict__ count) {
+  extern __shared__ uint16_t s_tab[];
+  uint16_t* s_t1 = s_tab;
+  uint16_t* s_t2p = s_tab + nstates * 8;
+  for (int i = threadIdx.x; i < nstates * 8; i += kBlock) s_t1[i] = t1g[i];
+  for (int i = threadIdx.x; i < nstates * 64; i += kBlock) {
+    // coordinate-major index p = x_j x_{j-1} y_j y_{j-1} z_j z_{j-1} <- octant-major o
+    const int p = i & 63;
+    const int o = (((p >> 5) & 1) << 5) | (((p >> 3) & 1) << 4) | (((p >> 1) & 1) << 3) |
+                  (((p >> 4) & 1) << 2) | (((p >> 2) & 1) << 1) | (p & 1);
+    s_t2p[i] = t2g[(i & ~63) + o];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t groups = (n + 3) >> 2;
+  const int64_t wstride = (int64_t)gridDim.x * (kBlock / 32) * 32;
+  for (int64_t g0 = ((int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5)) * 32; g0 < groups;
+       g0 += wstride) {
+    const int64_t g = g0 + lane;
+    const int64_t h0 = g * 4;
+    uint32_t xs[4] = {0, 0, 0, 0}, ys[4] = {0, 0, 0, 0}, zs[4] = {0, 0, 0, 0}, lv[4] = {0, 0, 0, 0};
+    int cnt = 0;
+    if (g < groups) {
+      cnt = (int)(n - h0 < 4 ? n - h0 : 4);
+      if (VEC && cnt == 4) {
+        const uint4* l4 = reinterpret_cast<const uint4*>(lower) + 3 * g;
+        const uint4 a = l4[0], bq = l4[1], c = l4[2];
+        const uint32_t L4 = reinterpret_cast<const uint32_t*>(level)[g];
+        xs[0] = a.x; ys[0] = a.y; zs[0] = a.z;
+        xs[1] = a.w; ys[1] = bq.x; zs[1] = bq.y;
+        xs[2] = bq.z; ys[2] = bq.w; zs[2] = c.x;
+        xs[3] = c.y; ys[3] = c.z; zs[3] = c.w;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) lv[i] = (L4 >> (8 * i)) & 255u;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool ok = i < cnt;
+          xs[i] = ok ? lower[3 * (h0 + i)] : 0u;
+          ys[i] = ok ? lower[3 * (h0 + i) + 1] : 0u;
+          zs[i] = ok ? lower[3 * (h0 + i) + 2] : 0u;
+          lv[i] = ok ? level[h0 + i] : 0u;
+        }
+      }
+    }
+    K code[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t half = (1u << lv[i]) >> 1;
+      code[i] = hilbert_code_cm<K>(xs[i] + half, ys[i] + half, zs[i] + half, b, s_t1, s_t2p);
+    }
+    if (cnt == 4) {
+      if (sizeof(K) == 4) {
+        reinterpret_cast<uint4*>(keys)[g] =
+            make_uint4((uint32_t)code[0], (uint32_t)code[1], (uint32_t)code[2], (uint32_t)code[3]);
+      } else {
+        ulonglong2* k2 = reinterpret_cast<ulonglong2*>(keys) + 2 * g;
+        k2[0] = make_ulonglong2(code[0], code[1]);
+        k2[1] = make_ulonglong2(code[2], code[3]);
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) keys[h0 + i] = code[i];
+    }
+    const uint32_t b0 = cnt ? (uint32_t)(code[0] >> lb) : 0xffffffffu;
+    const bool same = cnt == 4 && (uint32_t)(code[1] >> lb) == b0 && (uint32_t)(code[2] >> lb) == b0 &&
+                      (uint32_t)(code[3] >> lb) == b0;
+    uint32_t sl[4];
+    if (__all_sync(0xffffffffu, same || cnt == 0)) {   // every lane's four cells share a bucket
+      const uint32_t peers = __match_any_sync(0xffffffffu, b0);
+      uint32_t base = 0;
+      if (b0 != 0xffffffffu && (peers & lt) == 0) base = atomicAdd(count + b0, 4u * __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1) + 4u * __popc(peers & lt);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sl[i] = base + i;
+    } else {
+      uint32_t bkt[4], peers[4], base[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bkt[i] = i < cnt ? (uint32_t)(code[i] >> lb) : 0xffffffffu;
+        peers[i] = __match_any_sync(0xffffffffu, bkt[i]);
+        base[i] = 0;
+        if (bkt[i] != 0xffffffffu && (peers[i] & lt) == 0)
+          base[i] = atomicAdd(count + bkt[i], (uint32_t)__popc(peers[i]));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        sl[i] = __shfl_sync(0xffffffffu, base[i], __ffs(peers[i]) - 1) + __popc(peers[i] & lt);
+    }
+    if (cnt == 4) {
+      reinterpret_cast<uint2*>(slot)[g] = make_uint2((sl[0] & 0xffffu) | (sl[1] << 16),
+                                                     (sl[2] & 0xffffu) | (sl[3] << 16));
+    } else {
+      for (int i = 0; i < cnt; ++i) slot[h0 + i] = (uint16_t)sl[i];
+    }
+  }
+}
+
+void launch_encode_bucket(const uint32_t* lower, const uint8_t* level, int64_t n, int b, int lb,
+                          int key_bytes, const uint16_t* d_t1, const uint16_t* d_t2, int nstates,
+                          void* keys, uint16_t* slot, uint32_t* count, int num_sms, cudaStream_t st) {
+  const size_t smem = (size_t)nstates * (8 + 64) * sizeof(uint16_t);
+  const bool vec = (reinterpret_cast<uintptr_t>(lower) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(level) & 3) == 0;
+  const int64_t warps = ((n + 3) / 4 + 31) / 32;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)num_sms * 8));
+#define EB(K, V)                                                                               \
+  encode_bucket_kernel<K, V><<<grid, kBlock, smem, st>>>(lower, level, n, b, lb, d_t1, d_t2,   \
+                                                         nstates, (K*)keys, slot, count)
+  if (key_bytes == 4) {
+    if (vec) EB(uint32_t, true); else EB(uint32_t, false);
+  } else {
+    if (vec) EB(unsigned long long, true); else EB(unsigned long long, false);
+  }
+#undef EB
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kBlock)
 encode_hist_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restrict__ level,

@@ -462,3 +462,45 @@ def test_binding_validates_device_arguments(dvl):
     with pytest.raises(ValueError):
         ctx.get_polylines(64, out=torch.empty(2 * 64 * 8 - 1, dtype=torch.int32, device="cuda"))
     ctx.close()
+
+
+@pytest.mark.parametrize("sort", ["auto", "lsd"])
+@pytest.mark.parametrize("E,Lmax,n", [(2, 1, None), (8, 2, None), (64, 3, None), (512, 4, None),
+                                      (4096, 4, 50000)])
+def test_sort_paths(dvl, sort, E, Lmax, n):
+    """The bucket sort (3b <= 36) and the onesweep LSD sort give the oracle's order bit for
+    bit, from one-bucket grids (b = 1, 3) to 2^24 buckets (b = 12, u64 keys)."""
+    if n is None:
+        lower, level = octree(E, Lmax, E + Lmax)
+    else:
+        lower, level = sparse_cells(E, n, 5, Lmax=Lmax)
+    scal = scalars(len(level), 3, 9)
+    B = o.build(lower, level, scal)
+    ctx = dvl.Context(device=0, sort=sort)
+    ctx.build(lower, level, scal)
+    check_build(B, dict(sorted=ctx.get_sorted(), data=ctx.get_sorted_data(), info=ctx.info()))
+    ctx.close()
+
+
+@pytest.mark.parametrize("sort", ["auto", "lsd"])
+def test_duplicate_and_overlap_detection_both_sorts(dvl, sort):
+    """Duplicates inside one bucket (bitmap and comparison ranks) and nested cells are
+    rejected with DVL_E_OVERLAP by either sort."""
+    lower, level = octree(64, 3, 12)
+    for dup in (0, 5):
+        lo2 = np.concatenate([lower, lower[dup:dup + 1]])
+        lv2 = np.concatenate([level, level[dup:dup + 1]])
+        ctx = dvl.Context(device=0, sort=sort)
+        with pytest.raises(dvl.DvlError) as e:
+            ctx.build(lo2, lv2, scalars(len(lv2), 2, 1))
+        assert e.value.status == "DVL_E_OVERLAP"
+        ctx.close()
+    # a level-0 cell inside a coarser one
+    big = np.nonzero(level > 0)[0][0]
+    lo3 = np.concatenate([lower, lower[big:big + 1]])
+    lv3 = np.concatenate([level, np.zeros(1, np.uint8)])
+    ctx = dvl.Context(device=0, sort=sort)
+    with pytest.raises(dvl.DvlError) as e:
+        ctx.build(lo3, lv3, scalars(len(lv3), 2, 1))
+    assert e.value.status == "DVL_E_OVERLAP"
+    ctx.close()
