@@ -11,8 +11,11 @@ flushed (256 MiB write) before every timed step.  Device time per step = CUDA ev
 the library's stream; per-kernel times come from the library's own events (same stream).
 
 --impl reference times the CPU oracle (oracle/, single thread) on the same config.
-N>1 (torchrun): every rank runs the workload on its own GPU (replicas, weak scaling);
-timing is the max over ranks.
+N>1 (torchrun): one context per GPU with the library's own NCCL communicator; dvl_build is
+the distributed Hilbert-key sample sort of round-robin input slices, every edit the sharded
+update (all_gather of the Q totals, MAX + SUM merge of the pixel accumulators).  --scaling
+weak (default): one config-sized piece per GPU; --scaling strong: the config split over the
+GPUs.  Timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -44,6 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded path (collectives) even at N=1")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = one config-sized piece per GPU; strong = the config "
+                         "split over the GPUs (C4 over 2/4/8, C5 over 8)")
     ap.add_argument("--also", default=None,
                     help="comma-separated extra configs measured after the main one (N=1, own "
                          "subprocess) and reported under 'also'; default C3 with C2; 'none'")
@@ -286,54 +292,73 @@ def run_native(args, rank, world, local):
 
     import synth
     dev = torch.device("cuda", local)
-    # sharded (N > 1): weak scaling over a 2x larger logical grid whose first `world`
-    # octants in curve order each hold one rank's config-sized piece -- every rank owns one
-    # contiguous range of the global Hilbert order (codes with one more bit)
-    c = device_workload(args.config, dev, synth.CELL_SEED + (rank if sharded else 0))
-    n = int(c["level"].shape[0])
+    strong = sharded and args.scaling == "strong"
+    gbits = 0
+    if not sharded:
+        c = device_workload(args.config, dev, synth.CELL_SEED)
+        lower_d, level_d, scal_d, domain = c["lower"], c["level"], c["scal"], c["domain"]
+        n_global = int(level_d.shape[0])
+    elif strong:
+        # strong scaling: one dataset (the config) over all ranks; every rank generates it
+        # (same seed, in HBM) and keeps the round-robin slice rank::world of the generator
+        # order as its build input, so the sample sort moves ~(G-1)/G of the cells
+        c = device_workload(args.config, dev, synth.CELL_SEED)
+        n_global = int(c["level"].shape[0])
+        lower_d = c["lower"][rank::world].contiguous()
+        level_d = c["level"][rank::world].contiguous()
+        scal_d = c["scal"][:, rank::world].contiguous()
+        domain = c["domain"]
+        del c
+    else:
+        # weak scaling: G config-sized pieces (seeds 2306 + p) in the first G curve-order
+        # octants of a grid with one more bit; every rank generates all pieces and keeps the
+        # round-robin slice of their concatenation as its build input
+        pieces, doms = [], []
+        for p in range(world):
+            cp = device_workload(args.config, dev, synth.CELL_SEED + p)
+            b0 = int(np.ceil(np.log2(cp["E"])))
+            gbits = b0 + 1
+            corners = np.array([[x, y, z] for x in (0, 1) for y in (0, 1) for z in (0, 1)],
+                               np.uint32) * np.uint32(1 << b0)
+            order = np.argsort(dvl.hilbert_encode_host(corners, gbits))
+            lo_p = cp["lower"] + torch.from_numpy(corners[order[p]].astype(np.int32)).to(dev)[None, :]
+            pieces.append((lo_p, cp["level"], cp["scal"]))
+            doms.append(cp["domain"])
+            c = cp
+        n_global = sum(int(pc[1].shape[0]) for pc in pieces)
+        lower_d = torch.cat([pc[0] for pc in pieces])[rank::world].contiguous()
+        level_d = torch.cat([pc[1] for pc in pieces])[rank::world].contiguous()
+        scal_d = torch.cat([pc[2] for pc in pieces], dim=1)[:, rank::world].contiguous()
+        domain = None if doms[0] is None else np.stack(
+            [np.minimum.reduce([d[:, 0] for d in doms]), np.maximum.reduce([d[:, 1] for d in doms])], 1)
+        del pieces
     M, W, N = c["M"], c["W"], 256
     base, edits = tf_sequence(args.config, args.warmup + args.steps, N, M)
-    gbits = 0
-    lower_d, level_d, scal_d = c["lower"], c["level"], c["scal"]
-    if sharded:
-        b0 = int(np.ceil(np.log2(c["E"])))
-        gbits = b0 + 1
-        half = np.uint32(1 << b0)
-        corners = np.array([[x, y, z] for x in (0, 1) for y in (0, 1) for z in (0, 1)], np.uint32) * half
-        order = np.argsort(dvl.hilbert_encode_host(corners, gbits))
-        lower_d = lower_d + torch.from_numpy(corners[order[rank]].astype(np.int32)).to(dev)[None, :]
 
     stream = torch.cuda.Stream()
     ctx = dvl.Context(device=local, stream=stream, timing=True)
-    if gbits:
-        ctx.set_global_bits(gbits)
-    n_global = n * world
     if sharded:
-        # the build's input is a round-robin slice of the global generator order (untimed
-        # setup), so the distributed sample sort really moves cells between the ranks
-        from paper_2306_11612_b200 import dist_build
-        coll = dist_build.TorchCollectives()
-        dst = torch.arange(n, device=dev) % world
-        order = torch.argsort(dst, stable=True)
-        cnt = torch.bincount(dst, minlength=world)
-        allc = torch.stack(coll.all_gather(cnt))
-        sendc, recvc = cnt.tolist(), allc[:, rank].tolist()
-        lower_d = coll.all_to_all(lower_d.reshape(-1, 3)[order], sendc, recvc)
-        level_d = coll.all_to_all(level_d[order], sendc, recvc)
-        scal_d = coll.all_to_all(scal_d[:, order].t().contiguous(), sendc, recvc).t().contiguous()
+        # the context's own NCCL communicator (libnccl.so.2 loaded by the library): dvl_build
+        # is then the distributed sample sort, dvl_get_polylines the sharded edit
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(dvl.dvl.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        ctx.set_comm(world, rank, bytes(uid.cpu().numpy().tobytes()))
+        if gbits:
+            ctx.set_global_bits(gbits)
     torch.cuda.synchronize()
 
     # ---- build (device-resident inputs), timed separately
     build_ms, phase = [], []
     for r in range(args.build_reps + 1):
         if sharded:
-            # distributed build: local sort, sample sort exchange over NCCL, local sort of
-            # the received key range (host-synchronising collectives: wall clock, max over
-            # ranks)
+            # distributed build inside the library (host-synchronising collectives: wall
+            # clock, max over ranks)
             dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            dinfo = dist_build.distributed_build(ctx, lower_d, level_d, scal_d, coll)
+            ctx.build(lower_d, level_d, scal_d)
             torch.cuda.synchronize()
             t = torch.tensor([1e3 * (time.perf_counter() - t0)], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -349,19 +374,8 @@ def run_native(args, rank, world, local):
             build_ms.append(ms_b)
             phase.append(ctx.timings())
     info = ctx.info()
-    domain = c["domain"]
+    n = int(info["n"])                     # this rank's cells (after the exchange)
     polylines = ctx.get_polylines
-    if sharded:
-        from paper_2306_11612_b200.shard import ShardedContext
-        sc = ShardedContext(ctx)
-        n = int(dinfo["n_local"])          # this rank's cells after the exchange
-        if domain is not None:   # shared domain: union over all ranks
-            d = torch.tensor(domain, device=dev)
-            lo_, hi_ = d[:, 0].contiguous(), d[:, 1].contiguous()
-            dist.all_reduce(lo_, op=dist.ReduceOp.MIN)
-            dist.all_reduce(hi_, op=dist.ReduceOp.MAX)
-            domain = torch.stack([lo_, hi_], 1).cpu().numpy()
-        polylines = sc.get_polylines
     for m in range(M):
         if domain is not None:
             ctx.set_domain(m, float(domain[m, 0]), float(domain[m, 1]))
@@ -499,12 +513,12 @@ def run_native(args, rank, world, local):
     pass_bytes = n * (bytes_cell["weights_scan_ms"] + bytes_cell["bin_reduce_ms"])
     update_kernels_ms = per_kernel["weights_scan_ms"] + per_kernel["bin_reduce_ms"]
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not sharded:
         try:
             cpu = cpu_baseline(c, base, W)
         except Exception as ex:  # pragma: no cover
             cpu = {"error": str(ex)}
-    del c, lower_d, level_d, scal_d
+    del lower_d, level_d, scal_d
     ctx.close()
     torch.cuda.empty_cache()
     also = {}
@@ -525,7 +539,7 @@ def run_native(args, rank, world, local):
     emit({
         "metric": METRIC, "value": value, "unit": "Gcells/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling if sharded else "weak", "vs_baseline": None,
         "dtype": "f32/u64", "data": "synthetic",
         "config": workload_config(args.config, n_global, M, W, N, int(info["Lmax"]) + 1, info["bits"], world,
                                   sharded, gbits, n_per_gpu=n_global // world),

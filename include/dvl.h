@@ -261,6 +261,37 @@ uint64_t dvl_shard_export_words(dvl_ctx *ctx, uint32_t W);
 dvl_status dvl_nccl_unique_id(void *id128);
 dvl_status dvl_set_comm(dvl_ctx *ctx, int nranks, int rank, const void *id128);
 
+/* An in-process group of nranks contexts (driven by nranks host threads of one process, on
+ * one or several devices): the same collectives as NCCL, done as device-to-device copies
+ * between the ranks' buffers with a host barrier.  It lets the whole distributed path run
+ * through this ABI on a single GPU (NCCL cannot place two ranks on one device).  The group
+ * handle is reference counted: destroy it whenever; the contexts keep their share. */
+dvl_status dvl_local_group_create(int nranks, void **group);
+void dvl_local_group_destroy(void *group);
+dvl_status dvl_set_local_comm(dvl_ctx *ctx, void *group, int rank);
+
+/* Distributed build (SURVEY 8(e) "Build"; the order of P:309-311 over all ranks).  When the
+ * context has a communicator (dvl_set_comm / dvl_set_local_comm), dvl_build is collective:
+ * every rank passes its own slice of the cells (any slice, possibly empty, same member
+ * count), and the library runs the Hilbert-key sample sort: all_reduce of the extent /
+ * Lmax / n (one global code width b), local encode + sort + gather, 1024 regular samples per
+ * rank all_gathered, G-1 splitters by dvl_select_splitters' rule, send ranges by binary
+ * search, the G x G counts all_gathered, the codes / global input ids / levels / member rows
+ * exchanged (grouped send / recv), the received sorted runs combined by the bucket placement
+ * of distinct codes, the dyadic overlap rule checked inside and across the rank
+ * boundaries, member ranges and offsets agreed.  Each rank then holds one contiguous range
+ * of the global curve order as a shard (dvl_get_shard), and dvl_get_polylines runs the
+ * sharded edit.  dvl_get_sorted returns the global input ids (the slices' concatenation in
+ * rank order).  All ranks return the same status. */
+dvl_status dvl_get_shard(dvl_ctx *ctx, dvl_shard_info *out);   /* vmin / vmax set to NULL */
+
+/* The sample sort's splitter rule, on the host: samples = nranks rows of per_rank codes
+ * (rank p's first min(per_rank, counts[p]) entries are its regular samples), counts[p] =
+ * cells of rank p.  Writes nranks-1 strictly increasing splitters (the weighted global
+ * quantiles k n / nranks).  Errors: INVAL (no strictly increasing choice exists). */
+dvl_status dvl_select_splitters(const uint64_t *samples, const uint64_t *counts, int nranks,
+                                int per_rank, uint64_t *splitters);
+
 /* Pass 2 of this shard (U3+U4) with the global scan offset and Qtot derived on the device
  * from totals_dev[nshards] (the gathered dvl_shard_total values, shard order), then export
  * of the per-pixel accumulators to export_dev (device, dvl_shard_export_words int64): the

@@ -26,6 +26,7 @@ struct Dataset {
   uint32_t E = 0;
   void* keys = nullptr;                 // sorted codes (n x key_bytes)
   uint32_t* perm = nullptr;             // input id of each sorted cell
+  unsigned long long* gids = nullptr;   // distributed build: global input id of each cell
   uint8_t* level_s = nullptr;           // n_pad
   float* scal_s = nullptr;              // M x n_pad
   std::vector<float> vmin, vmax;        // member data ranges (finite values)
@@ -112,9 +113,10 @@ struct dvl_ctx {
   int acc_par = 0;                        // which lo / hi copy the next call uses
   uint32_t acc_dirty[2] = {0, 0};         // per lo / hi copy: pixels [0, w) not yet restored
   bool volume = false;                    // dvl_set_level_scale: weights by cell volume
-  // dvl_set_comm: the context's own NCCL communicator over the shards; dvl_get_polylines
-  // then runs the sharded edit (both exchanges) itself
-  void* comm = nullptr;
+  // dvl_set_comm / dvl_set_local_comm: the context's own communicator over the shards;
+  // dvl_build then runs the distributed sample sort and dvl_get_polylines the sharded edit
+  // (both exchanges) itself
+  Comm* comm = nullptr;
   int comm_ranks = 0, comm_rank = 0;
   unsigned long long* d_totals = nullptr;   // [comm_ranks]
   int64_t* d_export = nullptr;              // the accumulator export, merged in place
@@ -207,7 +209,7 @@ void dfree(dvl_ctx* ctx, void* p) {
 }
 
 void free_dataset(dvl_ctx* ctx, Dataset& d) {
-  void* ps[] = {d.keys, d.perm, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
+  void* ps[] = {d.keys, d.perm, d.gids, d.level_s, d.scal_s, d.d_vmin, d.d_vmax, d.d_lo, d.d_inv,
                 d.d_rgba, d.d_tab, d.status1, d.tile_prefix, d.chunk_status, d.chunk_prefix,
                 d.tile_meta, d.meta2, d.agg, d.cmin, d.cmax, d.blist, d.bctr};
   for (void* p : ps) dfree(ctx, p);
@@ -661,7 +663,7 @@ void dvl_destroy(dvl_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  nccl_comm_destroy(ctx->comm);
+  delete ctx->comm;
   free_dataset(ctx, ctx->ds);
   std::vector<void*> ps;
   for (auto& kv : ctx->live) ps.push_back(kv.first);
@@ -677,240 +679,244 @@ void dvl_destroy(dvl_ctx* ctx) {
   delete ctx;
 }
 
-dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const uint8_t* level,
-                     uint32_t members, const float* const* scalars, dvl_mem where) {
-  if (!ctx) return DVL_E_INVAL;
-  ctx->err.clear();
+// ------------------------------------------------------------------ build helpers
+namespace {
 
-  Dataset d;
-  std::vector<void*> tmp;   // temporaries freed on every exit
-  auto cleanup = [&]() {
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (void* p : tmp) dfree(ctx, p);
-  };
-  try {
-    if (n == 0) fail(ctx, DVL_E_INVAL, "n must be >= 1");
-    if (n >= (1ull << 30)) fail(ctx, DVL_E_RANGE, "n must be < 2^30 per device");
-    if (members < 1 || members > (uint32_t)kMaxM) fail(ctx, DVL_E_INVAL, "members must be in [1, 64]");
-    if (!lower_xyz || !level || !scalars) fail(ctx, DVL_E_INVAL, "NULL input pointer");
-    for (uint32_t m = 0; m < members; ++m)
-      if (!scalars[m]) fail(ctx, DVL_E_INVAL, "NULL scalar pointer");
-    if (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE) fail(ctx, DVL_E_INVAL, "bad dvl_mem");
-    CK(cudaSetDevice(ctx->device));
-    const int M = (int)members;
-    const int64_t nn = (int64_t)n;
-    cudaStream_t st = ctx->stream;
+using Tmp = std::vector<void*>;
 
-    // ---- stage inputs on the device
-    const uint32_t* d_lower = lower_xyz;
-    const uint8_t* d_level = level;
-    std::vector<const float*> scal_ptrs(scalars, scalars + M);
-    tic(ctx, PH_INGEST);
-    if (where == DVL_MEM_HOST) {
-      uint32_t* l = dalloc<uint32_t>(ctx, 3 * (size_t)nn);
-      tmp.push_back(l);
-      uint8_t* lv = dalloc<uint8_t>(ctx, nn);
-      tmp.push_back(lv);
-      float* sc = dalloc<float>(ctx, (size_t)M * nn);
-      tmp.push_back(sc);
-      CK(cudaMemcpyAsync(l, lower_xyz, 12 * (size_t)nn, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(lv, level, nn, cudaMemcpyHostToDevice, st));
-      for (int m = 0; m < M; ++m) {
-        CK(cudaMemcpyAsync(sc + (size_t)m * nn, scalars[m], 4 * (size_t)nn, cudaMemcpyHostToDevice, st));
-        scal_ptrs[m] = sc + (size_t)m * nn;
-      }
-      d_lower = l;
-      d_level = lv;
-    }
-    const float** d_ptrs = (const float**)dmalloc(ctx, sizeof(float*) * M);
-    tmp.push_back((void*)d_ptrs);
-    CK(cudaMemcpyAsync(d_ptrs, scal_ptrs.data(), sizeof(float*) * M, cudaMemcpyHostToDevice, st));
+// device copies of the inputs (host inputs are staged into temporaries) and the device
+// array of the member row pointers
+struct Inputs {
+  const uint32_t* lower = nullptr;
+  const uint8_t* level = nullptr;
+  const float** d_ptrs = nullptr;
+};
 
-    // ---- B0: ingest reduction
-    IngestOut h_ing;
-    memset(&h_ing, 0, sizeof h_ing);
-    for (int m = 0; m < 64; ++m) h_ing.vmin[m] = 0xffffffffu;
-    IngestOut* d_ing = (IngestOut*)dmalloc(ctx, sizeof(IngestOut));
-    tmp.push_back(d_ing);
-    CK(cudaMemcpyAsync(d_ing, &h_ing, sizeof h_ing, cudaMemcpyHostToDevice, st));
-    int grid = (int)std::min<int64_t>((nn + kBlock - 1) / kBlock, 148 * 8);
-    // geometry only: the member ranges are folded into the gather (B3)
-    launch_ingest_geom(d_lower, d_level, nn, d_ing, ctx->num_sms, st);
-    CKLAUNCH();
-    toc(ctx, PH_INGEST);
-    CK(cudaMemcpyAsync(&h_ing, d_ing, sizeof h_ing, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (h_ing.err & kErrInval) fail(ctx, DVL_E_INVAL, "a cell has L > 20 or a lower corner not a multiple of 2^L");
-    if (h_ing.extent > (1ull << 21)) fail(ctx, DVL_E_RANGE, "logical extent E > 2^21");
-    if (ceil_lmax_p(lscale(ctx) * (int)h_ing.lmax, ctx->P) > 100)
-      fail(ctx, DVL_E_RANGE, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
-    d.n = nn;
-    d.M = M;
-    d.E = (uint32_t)h_ing.extent;
-    d.b = std::max(1, ceil_log2_u64(h_ing.extent));
-    if (ctx->global_bits > 0) {
-      if (d.b > ctx->global_bits) fail(ctx, DVL_E_RANGE, "shard extent exceeds 2^global_bits");
-      d.b = ctx->global_bits;
-    }
-    d.Lmax = (int)h_ing.lmax;
-    d.key_bytes = 3 * d.b <= 32 ? 4 : 8;
-    d.passes = (3 * d.b + 7) / 8;
-    d.tma = M <= 16 && !(ctx->flags & DVL_FLAG_GENERIC);
-    d.items = items_for(M, d.tma);
-    const int64_t T = (int64_t)kBlock * d.items;
-    d.tiles = (int)((nn + T - 1) / T);
-    d.n_pad = (int64_t)d.tiles * T;
-    // ---- B1: Hilbert encode (+ bucket counts or digit histograms)
-    const int kb = d.key_bytes;
-    void* kA = dmalloc(ctx, (size_t)kb * nn);
-    void* kB = dmalloc(ctx, (size_t)kb * nn);
-    uint32_t* iA = dalloc<uint32_t>(ctx, nn);
-    uint32_t* iB = dalloc<uint32_t>(ctx, nn);
-    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
-    const bool bucket = 3 * d.b <= 36 && !(ctx->flags & DVL_FLAG_LSD_SORT);
-    if (bucket) {
-      // B1 + B2 as the two-pass bucket sort of distinct codes (bsort.cu)
-      int lb = 0;
-      const int64_t nb = bucket_count(d.b, &lb);
-      const int64_t nblk = (nb + 4095) / 4096;
-      uint32_t* bcnt = dalloc<uint32_t>(ctx, (size_t)nb);
-      uint32_t* bstart = dalloc<uint32_t>(ctx, (size_t)nb + 1);
-      uint16_t* slot = dalloc<uint16_t>(ctx, (size_t)nn);
-      uint32_t* bsum = dalloc<uint32_t>(ctx, (size_t)nblk + 1);
-      uint32_t* work = dalloc<uint32_t>(ctx, 1);
-      tmp.push_back(bcnt);
-      tmp.push_back(bstart);
-      tmp.push_back(slot);
-      tmp.push_back(bsum);
-      tmp.push_back(work);
-      CK(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * nb, st));
-      CK(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));
-      tic(ctx, PH_ENCODE);
-      launch_encode_bucket(d_lower, d_level, nn, d.b, lb, kb, ctx->d_t1, ctx->d_t2, ctx->nstates,
-                           kA, slot, bcnt, ctx->num_sms, st);
-      CKLAUNCH();
-      toc(ctx, PH_ENCODE);
-      tic(ctx, PH_SORT);
-      launch_bucket_scan(bcnt, nb, lb, bsum, bstart, (uint32_t)nn, ctx->d_err, st);
-      CKLAUNCH();
-      launch_bucket_sort(kA, slot, kb, nn, lb, nb, bstart, kB, iB, kA, iA, work, ctx->d_err,
-                         ctx->num_sms, st);
-      CKLAUNCH();
-      toc(ctx, PH_SORT);
-      ctx->sort_passes = 2;
-      d.keys = kA;
-      d.perm = iA;
-      tmp.push_back(kB);
-      tmp.push_back(iB);
-    } else {
-      uint32_t* hist = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
-      uint32_t* base = dalloc<uint32_t>(ctx, (size_t)d.passes * 256);
-      const int64_t stiles = (nn + kSortTile - 1) / kSortTile;
-      uint32_t* status = dalloc<uint32_t>(ctx, (size_t)d.passes * stiles * 256);
-      uint32_t* ctrs = dalloc<uint32_t>(ctx, d.passes);
-      tmp.push_back(hist);
-      tmp.push_back(base);
-      tmp.push_back(status);
-      tmp.push_back(ctrs);
-      CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * d.passes * 256, st));
-      CK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * d.passes * stiles * 256, st));
-      CK(cudaMemsetAsync(ctrs, 0, sizeof(uint32_t) * d.passes, st));
-      tic(ctx, PH_ENCODE);
-      launch_encode_hist(d_lower, d_level, nn, d.b, kb, d.passes, ctx->d_t1, ctx->d_t2,
-                         ctx->nstates, kA, iA, hist, grid, st);
-      CKLAUNCH();
-      toc(ctx, PH_ENCODE);
-
-      // ---- B2: onesweep passes (a pass whose digit is constant is the identity: skipped)
-      tic(ctx, PH_SORT);
-      launch_hist_scan(hist, base, d.passes, st);
-      CKLAUNCH();
-      std::vector<uint32_t> h_hist((size_t)d.passes * 256);
-      CK(cudaMemcpyAsync(h_hist.data(), hist, 4 * h_hist.size(), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      void* kin = kA;
-      void* kout = kB;
-      uint32_t* vin = iA;
-      uint32_t* vout = iB;
-      int done = 0;
-      for (int p = 0; p < d.passes; ++p) {
-        uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
-        if ((int64_t)mx == nn) continue;
-        // the first pass generates the ids (iota) instead of reading them
-        launch_onesweep(kin, done == 0 ? nullptr : vin, kout, vout, nn, kb, 8 * p, base + p * 256,
-                        status + (size_t)p * stiles * 256, ctrs + p, st);
-        CKLAUNCH();
-        std::swap(kin, kout);
-        std::swap(vin, vout);
-        ++done;
-      }
-      if (done == 0) {   // every digit constant (n == 1): the identity permutation
-        launch_iota(vin, nn, st);
-        CKLAUNCH();
-      }
-      ctx->sort_passes = done;
-      toc(ctx, PH_SORT);
-      d.keys = kin;
-      d.perm = vin;
-      tmp.push_back(kout);
-      tmp.push_back(vout);
-    }
-
-    // ---- B3: permute into curve order + overlap validation
-    d.level_s = dalloc<uint8_t>(ctx, d.n_pad);
-    d.scal_s = dalloc<float>(ctx, (size_t)M * d.n_pad);
-    CK(cudaMemsetAsync(d.level_s, 0, d.n_pad, st));
-    CK(cudaMemsetAsync(d.scal_s, 0, sizeof(float) * M * d.n_pad, st));
-    tic(ctx, PH_GATHER);
-    launch_gather_validate4(d.keys, kb, d.perm, d_level, d_ptrs, nn, M, d.n_pad, d.level_s,
-                            d.scal_s, ctx->d_err, d_ing, ctx->num_sms, st);
-    CKLAUNCH();
-    toc(ctx, PH_GATHER);
-    uint32_t herr = 0;
-    CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&h_ing, d_ing, sizeof h_ing, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (herr & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
-    d.vmin.resize(M);
-    d.vmax.resize(M);
+Inputs stage_inputs(dvl_ctx* ctx, int64_t nn, const uint32_t* lower_xyz, const uint8_t* level,
+                    int M, const float* const* scalars, dvl_mem where, Tmp& tmp) {
+  cudaStream_t st = ctx->stream;
+  Inputs in;
+  in.lower = lower_xyz;
+  in.level = level;
+  std::vector<const float*> ptrs(M, nullptr);
+  if (scalars)
+    for (int m = 0; m < M; ++m) ptrs[m] = scalars[m];
+  if (where == DVL_MEM_HOST && nn > 0) {
+    uint32_t* l = dalloc<uint32_t>(ctx, 3 * (size_t)nn);
+    tmp.push_back(l);
+    uint8_t* lv = dalloc<uint8_t>(ctx, nn);
+    tmp.push_back(lv);
+    float* sc = dalloc<float>(ctx, (size_t)M * nn);
+    tmp.push_back(sc);
+    CK(cudaMemcpyAsync(l, lower_xyz, 12 * (size_t)nn, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(lv, level, nn, cudaMemcpyHostToDevice, st));
     for (int m = 0; m < M; ++m) {
-      d.vmin[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmin[m]) : 0.0f;
-      d.vmax[m] = h_ing.any[m] ? ordered_to_float(h_ing.vmax[m]) : 0.0f;
+      CK(cudaMemcpyAsync(sc + (size_t)m * nn, scalars[m], 4 * (size_t)nn, cudaMemcpyHostToDevice, st));
+      ptrs[m] = sc + (size_t)m * nn;
     }
-
-    // ---- per-dataset update state
-    d.d_vmin = dalloc<float>(ctx, M);
-    d.d_vmax = dalloc<float>(ctx, M);
-    d.d_lo = dalloc<float>(ctx, M);
-    d.d_inv = dalloc<float>(ctx, M);
-    d.d_rgba = dalloc<float4>(ctx, (size_t)M * kMaxN);
-    d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
-    d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
-    d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
-    if (d.tma) {
-      d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
-      d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
-      d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
-      d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
-      d.bctr = dalloc<uint32_t>(ctx, 2);
-      CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), st));
-    }
-    CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
-  } catch (Fail& f) {
-    cleanup();
-    free_dataset(ctx, d);
-    return f.s;
+    in.lower = l;
+    in.level = lv;
   }
-  cleanup();
-  // commit: replace the old dataset
+  in.d_ptrs = (const float**)dmalloc(ctx, sizeof(float*) * M);
+  tmp.push_back((void*)in.d_ptrs);
+  CK(cudaMemcpyAsync(in.d_ptrs, ptrs.data(), sizeof(float*) * M, cudaMemcpyHostToDevice, st));
+  return in;
+}
+
+IngestOut* new_ingest(dvl_ctx* ctx, Tmp& tmp) {
+  IngestOut h;
+  memset(&h, 0, sizeof h);
+  for (int m = 0; m < 64; ++m) h.vmin[m] = 0xffffffffu;
+  IngestOut* d = (IngestOut*)dmalloc(ctx, sizeof(IngestOut));
+  tmp.push_back(d);
+  CK(cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  return d;
+}
+
+void read_ingest(dvl_ctx* ctx, const IngestOut* d, IngestOut* h) {
+  CK(cudaMemcpyAsync(h, d, sizeof(IngestOut), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+
+struct Sorted {
+  void* keys = nullptr;      // n sorted codes (key_bytes each)
+  uint32_t* perm = nullptr;  // source index of each sorted code
+};
+
+// B2 on codes already in `keys` (n of them, b bits): the bucket sort of distinct codes for
+// 3b <= 36 (bsort.cu) or the onesweep LSD sort; with lower/level given, B1 (the Hilbert
+// encode) runs first and writes `keys` itself.  The returned arrays are owned by the
+// caller (the codes may end in `keys` or in a new buffer); the other temporaries go to tmp.
+Sorted sort_codes(dvl_ctx* ctx, const uint32_t* lower, const uint8_t* level, void* keys,
+                  int64_t nn, int b, int kb, Tmp& tmp) {
+  cudaStream_t st = ctx->stream;
+  const bool encode = lower != nullptr;
+  void* kA = keys;
+  void* kB = dmalloc(ctx, (size_t)kb * nn);
+  uint32_t* iA = dalloc<uint32_t>(ctx, nn);
+  uint32_t* iB = dalloc<uint32_t>(ctx, nn);
+  Sorted out;
+  const bool bucket = 3 * b <= 36 && !(ctx->flags & DVL_FLAG_LSD_SORT);
+  if (bucket) {
+    int lb = 0;
+    const int64_t nb = bucket_count(b, &lb);
+    const int64_t nblk = (nb + 4095) / 4096;
+    uint32_t* bcnt = dalloc<uint32_t>(ctx, (size_t)nb);
+    uint32_t* bstart = dalloc<uint32_t>(ctx, (size_t)nb + 1);
+    uint16_t* slot = dalloc<uint16_t>(ctx, (size_t)nn);
+    uint32_t* bsum = dalloc<uint32_t>(ctx, (size_t)nblk + 1);
+    uint32_t* work = dalloc<uint32_t>(ctx, 1);
+    for (void* q : {(void*)bcnt, (void*)bstart, (void*)slot, (void*)bsum, (void*)work}) tmp.push_back(q);
+    CK(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * nb, st));
+    CK(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));
+    tic(ctx, PH_ENCODE);
+    if (encode)
+      launch_encode_bucket(lower, level, nn, b, lb, kb, ctx->d_t1, ctx->d_t2, ctx->nstates, kA,
+                           slot, bcnt, ctx->num_sms, st);
+    else
+      launch_bucket_slot(kA, kb, nn, lb, slot, bcnt, ctx->num_sms, st);
+    CKLAUNCH();
+    toc(ctx, PH_ENCODE);
+    tic(ctx, PH_SORT);
+    launch_bucket_scan(bcnt, nb, lb, bsum, bstart, (uint32_t)nn, ctx->d_err, st);
+    CKLAUNCH();
+    launch_bucket_sort(kA, slot, kb, nn, lb, nb, bstart, kB, iB, kA, iA, work, ctx->d_err,
+                       ctx->num_sms, st);
+    CKLAUNCH();
+    toc(ctx, PH_SORT);
+    ctx->sort_passes = 2;
+    out.keys = kA;
+    out.perm = iA;
+    tmp.push_back(kB);
+    tmp.push_back(iB);
+    return out;
+  }
+  const int passes = (3 * b + 7) / 8;
+  uint32_t* hist = dalloc<uint32_t>(ctx, (size_t)passes * 256);
+  uint32_t* base = dalloc<uint32_t>(ctx, (size_t)passes * 256);
+  const int64_t stiles = (nn + kSortTile - 1) / kSortTile;
+  uint32_t* status = dalloc<uint32_t>(ctx, (size_t)passes * stiles * 256);
+  uint32_t* ctrs = dalloc<uint32_t>(ctx, passes);
+  for (void* q : {(void*)hist, (void*)base, (void*)status, (void*)ctrs}) tmp.push_back(q);
+  CK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * passes * 256, st));
+  CK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * passes * stiles * 256, st));
+  CK(cudaMemsetAsync(ctrs, 0, sizeof(uint32_t) * passes, st));
+  tic(ctx, PH_ENCODE);
+  const int grid = (int)std::min<int64_t>((nn + kBlock - 1) / kBlock, 148 * 8);
+  if (encode)
+    launch_encode_hist(lower, level, nn, b, kb, passes, ctx->d_t1, ctx->d_t2, ctx->nstates, kA,
+                       iA, hist, grid, st);
+  else
+    launch_key_hist(kA, kb, nn, passes, hist, ctx->num_sms, st);
+  CKLAUNCH();
+  toc(ctx, PH_ENCODE);
+  // onesweep passes (a pass whose digit is constant is the identity: skipped)
+  tic(ctx, PH_SORT);
+  launch_hist_scan(hist, base, passes, st);
+  CKLAUNCH();
+  std::vector<uint32_t> h_hist((size_t)passes * 256);
+  CK(cudaMemcpyAsync(h_hist.data(), hist, 4 * h_hist.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  void* kin = kA;
+  void* kout = kB;
+  uint32_t* vin = iA;
+  uint32_t* vout = iB;
+  int done = 0;
+  for (int p = 0; p < passes; ++p) {
+    uint32_t mx = *std::max_element(h_hist.begin() + p * 256, h_hist.begin() + (p + 1) * 256);
+    if ((int64_t)mx == nn) continue;
+    // the first pass generates the ids (iota) instead of reading them
+    launch_onesweep(kin, done == 0 ? nullptr : vin, kout, vout, nn, kb, 8 * p, base + p * 256,
+                    status + (size_t)p * stiles * 256, ctrs + p, st);
+    CKLAUNCH();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+    ++done;
+  }
+  if (done == 0) {   // every digit constant (n == 1): the identity permutation
+    launch_iota(vin, nn, st);
+    CKLAUNCH();
+  }
+  ctx->sort_passes = done;
+  toc(ctx, PH_SORT);
+  out.keys = kin;
+  out.perm = vin;
+  if (kout != keys) tmp.push_back(kout);   // the caller's buffer stays the caller's
+  tmp.push_back(vout);
+  return out;
+}
+
+// B3: level_s / scal_s (rows of n_pad) in sorted order from the source arrays through
+// `perm`, the overlap check along the run (error word) and the member ranges (into ing)
+void gather_sorted(dvl_ctx* ctx, Dataset& d, const uint8_t* level_in, const float* const* d_ptrs,
+                   IngestOut* ing) {
+  cudaStream_t st = ctx->stream;
+  d.level_s = dalloc<uint8_t>(ctx, d.n_pad);
+  d.scal_s = dalloc<float>(ctx, (size_t)d.M * d.n_pad);
+  CK(cudaMemsetAsync(d.level_s, 0, d.n_pad, st));
+  CK(cudaMemsetAsync(d.scal_s, 0, sizeof(float) * d.M * d.n_pad, st));
+  tic(ctx, PH_GATHER);
+  launch_gather_validate4(d.keys, d.key_bytes, d.perm, level_in, d_ptrs, d.n, d.M, d.n_pad,
+                          d.level_s, d.scal_s, ctx->d_err, ing, ctx->num_sms, st);
+  CKLAUNCH();
+  toc(ctx, PH_GATHER);
+}
+
+// tile geometry of a dataset of d.n cells and d.M members
+void set_geometry(dvl_ctx* ctx, Dataset& d) {
+  d.key_bytes = 3 * d.b <= 32 ? 4 : 8;
+  d.passes = (3 * d.b + 7) / 8;
+  d.tma = d.M <= 16 && !(ctx->flags & DVL_FLAG_GENERIC);
+  d.items = items_for(d.M, d.tma);
+  const int64_t T = (int64_t)kBlock * d.items;
+  d.tiles = (int)((d.n + T - 1) / T);
+  d.n_pad = (int64_t)d.tiles * T;
+}
+
+void ranges_from(Dataset& d, const IngestOut& h) {
+  d.vmin.resize(d.M);
+  d.vmax.resize(d.M);
+  for (int m = 0; m < d.M; ++m) {
+    d.vmin[m] = h.any[m] ? ordered_to_float(h.vmin[m]) : 0.0f;
+    d.vmax[m] = h.any[m] ? ordered_to_float(h.vmax[m]) : 0.0f;
+  }
+}
+
+// the per-dataset update state (TF tables, look-back state, D3 statistics, lists)
+void alloc_update_state(dvl_ctx* ctx, Dataset& d) {
+  cudaStream_t st = ctx->stream;
+  const int M = d.M;
+  d.d_vmin = dalloc<float>(ctx, M);
+  d.d_vmax = dalloc<float>(ctx, M);
+  d.d_lo = dalloc<float>(ctx, M);
+  d.d_inv = dalloc<float>(ctx, M);
+  d.d_rgba = dalloc<float4>(ctx, (size_t)M * kMaxN);
+  d.d_tab = dalloc<float2>(ctx, (size_t)M * kMaxN);
+  d.status1 = dalloc<unsigned long long>(ctx, d.tiles);
+  d.tile_prefix = dalloc<unsigned long long>(ctx, d.tiles);
+  if (d.tma) {
+    d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+    d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
+    d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
+    d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
+    d.bctr = dalloc<uint32_t>(ctx, 2);
+    CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), st));
+  }
+  CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));
+}
+
+// replace the context's dataset with d; default domains = the data ranges, identity TFs,
+// the first weights
+dvl_status commit_dataset(dvl_ctx* ctx, Dataset& d, bool sharded, uint64_t cell_offset,
+                          uint64_t n_global, int lmax_global) {
   free_dataset(ctx, ctx->ds);
   ctx->ds = d;
   ctx->built = true;
-  ctx->sharded = false;
-  ctx->cell_offset = 0;
-  ctx->n_global = (uint64_t)d.n;
-  ctx->lmax_global = d.Lmax;
+  ctx->sharded = sharded;
+  ctx->cell_offset = cell_offset;
+  ctx->n_global = n_global;
+  ctx->lmax_global = lmax_global;
   ctx->N = 256;
   ctx->lo_h = ctx->ds.vmin;
   ctx->hi_h = ctx->ds.vmax;
@@ -934,6 +940,410 @@ dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const 
   }
   return DVL_OK;
 }
+
+uint32_t read_err(dvl_ctx* ctx) {
+  uint32_t herr = 0;
+  CK(cudaMemcpyAsync(&herr, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return herr;
+}
+
+dvl_status dist_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const uint8_t* level,
+                      uint32_t members, const float* const* scalars, dvl_mem where);
+
+}  // namespace
+
+dvl_status dvl_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const uint8_t* level,
+                     uint32_t members, const float* const* scalars, dvl_mem where) {
+  if (!ctx) return DVL_E_INVAL;
+  ctx->err.clear();
+  if (ctx->comm) return dist_build(ctx, n, lower_xyz, level, members, scalars, where);
+
+  Dataset d;
+  Tmp tmp;   // temporaries freed on every exit
+  auto cleanup = [&]() {
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (void* p : tmp) dfree(ctx, p);
+  };
+  try {
+    if (n == 0) fail(ctx, DVL_E_INVAL, "n must be >= 1");
+    if (n >= (1ull << 30)) fail(ctx, DVL_E_RANGE, "n must be < 2^30 per device");
+    if (members < 1 || members > (uint32_t)kMaxM) fail(ctx, DVL_E_INVAL, "members must be in [1, 64]");
+    if (!lower_xyz || !level || !scalars) fail(ctx, DVL_E_INVAL, "NULL input pointer");
+    for (uint32_t m = 0; m < members; ++m)
+      if (!scalars[m]) fail(ctx, DVL_E_INVAL, "NULL scalar pointer");
+    if (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE) fail(ctx, DVL_E_INVAL, "bad dvl_mem");
+    CK(cudaSetDevice(ctx->device));
+    const int M = (int)members;
+    const int64_t nn = (int64_t)n;
+    cudaStream_t st = ctx->stream;
+
+    // ---- stage inputs; B0: ingest reduction over the geometry
+    tic(ctx, PH_INGEST);
+    Inputs in = stage_inputs(ctx, nn, lower_xyz, level, M, scalars, where, tmp);
+    IngestOut* d_ing = new_ingest(ctx, tmp);
+    launch_ingest_geom(in.lower, in.level, nn, d_ing, ctx->num_sms, st);
+    CKLAUNCH();
+    toc(ctx, PH_INGEST);
+    IngestOut h_ing;
+    read_ingest(ctx, d_ing, &h_ing);
+    if (h_ing.err & kErrInval) fail(ctx, DVL_E_INVAL, "a cell has L > 20 or a lower corner not a multiple of 2^L");
+    if (h_ing.extent > (1ull << 21)) fail(ctx, DVL_E_RANGE, "logical extent E > 2^21");
+    if (ceil_lmax_p(lscale(ctx) * (int)h_ing.lmax, ctx->P) > 100)
+      fail(ctx, DVL_E_RANGE, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
+    d.n = nn;
+    d.M = M;
+    d.E = (uint32_t)h_ing.extent;
+    d.b = std::max(1, ceil_log2_u64(h_ing.extent));
+    if (ctx->global_bits > 0) {
+      if (d.b > ctx->global_bits) fail(ctx, DVL_E_RANGE, "shard extent exceeds 2^global_bits");
+      d.b = ctx->global_bits;
+    }
+    d.Lmax = (int)h_ing.lmax;
+    set_geometry(ctx, d);
+
+    // ---- B1 + B2: Hilbert encode and sort
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
+    void* keys = dmalloc(ctx, (size_t)d.key_bytes * nn);
+    tmp.push_back(keys);
+    Sorted srt = sort_codes(ctx, in.lower, in.level, keys, nn, d.b, d.key_bytes, tmp);
+    if (srt.keys == keys) tmp.erase(std::find(tmp.begin(), tmp.end(), keys));
+    d.keys = srt.keys;
+    d.perm = srt.perm;
+
+    // ---- B3: permute into curve order + overlap validation + member ranges
+    gather_sorted(ctx, d, in.level, in.d_ptrs, d_ing);
+    const uint32_t herr = read_err(ctx);
+    read_ingest(ctx, d_ing, &h_ing);
+    if (herr & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
+    ranges_from(d, h_ing);
+    alloc_update_state(ctx, d);
+  } catch (Fail& f) {
+    cleanup();
+    free_dataset(ctx, d);
+    return f.s;
+  }
+  cleanup();
+  return commit_dataset(ctx, d, false, 0, (uint64_t)d.n, d.Lmax);
+}
+
+namespace {
+
+// the in-process stand-in for a communicator handle (dvl_local_group_create)
+struct GroupHandle {
+  LocalGroup* g;
+};
+
+void attach_comm(dvl_ctx* ctx, Comm* c) {
+  dfree(ctx, ctx->d_totals);
+  ctx->d_totals = dalloc<unsigned long long>(ctx, (size_t)c->nranks);
+  ctx->comm = c;
+  ctx->comm_ranks = c->nranks;
+  ctx->comm_rank = c->rank;
+}
+
+// a collective helper: small u64 vectors through device memory
+struct Small {
+  dvl_ctx* ctx;
+  unsigned long long* d = nullptr;
+  size_t cap = 0;
+  Small(dvl_ctx* c, size_t words) : ctx(c), cap(words) { d = dalloc<unsigned long long>(ctx, words); }
+  ~Small() { dfree(ctx, d); }
+  void put(const std::vector<uint64_t>& v) {
+    CK(cudaMemcpyAsync(d, v.data(), 8 * v.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  std::vector<uint64_t> get(size_t words) {
+    std::vector<uint64_t> v(words);
+    CK(cudaMemcpyAsync(v.data(), d, 8 * words, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return v;
+  }
+};
+
+void comm_ck(dvl_ctx* ctx, const char* e, const char* what) {
+  if (e) fail(ctx, DVL_E_NCCL, std::string(what) + ": " + e);
+}
+
+// error agreement: every rank learns the largest local status, so all ranks fail together
+// (a rank must never leave the others waiting in a collective)
+dvl_status agree(dvl_ctx* ctx, dvl_status local, const std::string& msg) {
+  Small sm(ctx, 1);
+  sm.put({(uint64_t)local});
+  comm_ck(ctx, ctx->comm->allreduce(sm.d, 1, kU64, kMax, ctx->stream), "status all_reduce");
+  const dvl_status g = (dvl_status)sm.get(1)[0];
+  if (g != DVL_OK) fail(ctx, g, local != DVL_OK ? msg : "another rank failed: " + std::string(dvl_status_string(g)));
+  return g;
+}
+
+// SURVEY 8(e) "Build": the Hilbert-key sample sort across the communicator's ranks.  Each
+// rank passes its slice of the cells (any slice, possibly empty); each ends with one
+// contiguous range of the global curve order, built and described as a shard.
+dvl_status dist_build(dvl_ctx* ctx, uint64_t n, const uint32_t* lower_xyz, const uint8_t* level,
+                      uint32_t members, const float* const* scalars, dvl_mem where) {
+  Comm& C = *ctx->comm;
+  const int G = C.nranks, r = C.rank;
+  Dataset d;
+  Tmp tmp;
+  auto cleanup = [&]() {
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (void* p : tmp) dfree(ctx, p);
+  };
+  uint64_t cell_offset = 0, n_global = 0;
+  int lmax_global = 0;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t nl = (int64_t)n;
+    const int M = (int)members;
+    // local argument errors join the first agreement
+    dvl_status argst = DVL_OK;
+    std::string argmsg;
+    if (n >= (1ull << 30)) { argst = DVL_E_RANGE; argmsg = "n must be < 2^30 per device"; }
+    if (members < 1 || members > (uint32_t)kMaxM) { argst = DVL_E_INVAL; argmsg = "members must be in [1, 64]"; }
+    if (n > 0 && (!lower_xyz || !level || !scalars)) { argst = DVL_E_INVAL; argmsg = "NULL input pointer"; }
+    if (where != DVL_MEM_HOST && where != DVL_MEM_DEVICE) { argst = DVL_E_INVAL; argmsg = "bad dvl_mem"; }
+    if (argst == DVL_OK && n > 0)
+      for (uint32_t m = 0; m < members; ++m)
+        if (!scalars[m]) { argst = DVL_E_INVAL; argmsg = "NULL scalar pointer"; }
+    agree(ctx, argst, argmsg);
+
+    // ---- 0. ingest of the local slice; global extent, Lmax, n, M (all ranks must agree)
+    tic(ctx, PH_INGEST);
+    Inputs in = stage_inputs(ctx, nl, lower_xyz, level, M, scalars, where, tmp);
+    IngestOut* d_ing = new_ingest(ctx, tmp);
+    if (nl > 0) {
+      launch_ingest_geom(in.lower, in.level, nl, d_ing, ctx->num_sms, st);
+      CKLAUNCH();
+    }
+    toc(ctx, PH_INGEST);
+    IngestOut h_ing;
+    read_ingest(ctx, d_ing, &h_ing);
+    {
+      Small mx(ctx, 4), sm(ctx, 2);
+      mx.put({h_ing.extent, h_ing.lmax, h_ing.err, (uint64_t)M});
+      sm.put({(uint64_t)nl, (uint64_t)M});
+      comm_ck(ctx, C.allreduce(mx.d, 4, kU64, kMax, st), "all_reduce MAX");
+      comm_ck(ctx, C.allreduce(sm.d, 2, kU64, kSum, st), "all_reduce SUM");
+      const std::vector<uint64_t> a = mx.get(4), b = sm.get(2);
+      if (a[2] & kErrInval) fail(ctx, DVL_E_INVAL, "a cell has L > 20 or a lower corner not a multiple of 2^L");
+      if (b[1] != (uint64_t)G * (uint64_t)M || a[3] != (uint64_t)M)
+        fail(ctx, DVL_E_INVAL, "the ranks pass different member counts");
+      if (b[0] == 0) fail(ctx, DVL_E_INVAL, "no cells on any rank");
+      if (a[0] > (1ull << 21)) fail(ctx, DVL_E_RANGE, "logical extent E > 2^21");
+      if (ceil_lmax_p(lscale(ctx) * (int)a[1], ctx->P) > 100)
+        fail(ctx, DVL_E_RANGE, "ceil(Lmax * P) > 100 (fp32 weight overflow)");
+      n_global = b[0];
+      lmax_global = (int)a[1];
+      d.b = std::max(1, ceil_log2_u64(a[0]));
+      if (ctx->global_bits > 0) d.b = std::max(d.b, ctx->global_bits);
+    }
+    d.M = M;
+    d.E = (uint32_t)h_ing.extent;
+    const int kb = 3 * d.b <= 32 ? 4 : 8;
+    // input offsets of the slices (global input ids = offset + local id)
+    std::vector<uint64_t> nin(G);
+    {
+      Small one(ctx, 1), all(ctx, G);
+      one.put({(uint64_t)nl});
+      comm_ck(ctx, C.allgather(one.d, all.d, 8, st), "all_gather n");
+      nin = all.get(G);
+    }
+    uint64_t in_offset = 0;
+    for (int p = 0; p < r; ++p) in_offset += nin[p];
+
+    // ---- 1. local encode + sort, gather into curve-ordered SoA (+ global ids)
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
+    const int64_t nl8 = (nl + 7) & ~7ll;
+    void* keys_l = dmalloc(ctx, (size_t)kb * std::max<int64_t>(nl, 1));
+    tmp.push_back(keys_l);
+    unsigned long long* ids_l = dalloc<unsigned long long>(ctx, std::max<int64_t>(nl, 1));
+    uint8_t* lev_l = dalloc<uint8_t>(ctx, std::max<int64_t>(nl8, 8));
+    float* sc_l = dalloc<float>(ctx, (size_t)M * std::max<int64_t>(nl8, 8));
+    tmp.push_back(ids_l);
+    tmp.push_back(lev_l);
+    tmp.push_back(sc_l);
+    Sorted loc;
+    if (nl > 0) {
+      loc = sort_codes(ctx, in.lower, in.level, keys_l, nl, d.b, kb, tmp);
+      if (loc.keys != keys_l) tmp.push_back(loc.keys);
+      tmp.push_back(loc.perm);
+      Dataset t;
+      t.n = nl;
+      t.n_pad = nl8;
+      t.M = M;
+      t.key_bytes = kb;
+      t.keys = loc.keys;
+      t.perm = loc.perm;
+      t.level_s = lev_l;
+      t.scal_s = sc_l;
+      launch_gather_validate4(t.keys, kb, t.perm, in.level, in.d_ptrs, nl, M, nl8, lev_l, sc_l,
+                              ctx->d_err, d_ing, ctx->num_sms, st);
+      CKLAUNCH();
+      launch_offset_ids(loc.perm, nl, in_offset, ids_l, ctx->num_sms, st);
+      CKLAUNCH();
+    }
+    const void* skeys = nl > 0 ? loc.keys : keys_l;
+
+    // ---- 2. samples -> splitters (identical on every rank)
+    constexpr int S = 1024;
+    std::vector<uint64_t> spl(std::max(G - 1, 1));
+    {
+      Small samp(ctx, S), all(ctx, (size_t)G * S);
+      launch_sample_keys(skeys, kb, nl, S, samp.d, st);
+      CKLAUNCH();
+      comm_ck(ctx, C.allgather(samp.d, all.d, 8 * S, st), "all_gather samples");
+      const std::vector<uint64_t> hs = all.get((size_t)G * S);
+      if (G > 1 && !select_splitters(hs.data(), nin.data(), G, S, spl.data()))
+        fail(ctx, DVL_E_INVAL, "fewer distinct cells than ranks: no valid splitters");
+    }
+    // ---- 3. send ranges (lower_bound of each splitter), the G x G count matrix
+    std::vector<uint64_t> bnd(G + 1, 0);
+    bnd[G] = (uint64_t)nl;
+    if (G > 1 && nl > 0) {
+      Small ds(ctx, G - 1), db(ctx, G - 1);
+      ds.put(std::vector<uint64_t>(spl.begin(), spl.begin() + (G - 1)));
+      launch_lower_bounds(skeys, kb, nl, ds.d, G - 1, db.d, st);
+      CKLAUNCH();
+      const std::vector<uint64_t> lb = db.get(G - 1);
+      for (int p = 1; p < G; ++p) bnd[p] = lb[p - 1];
+    } else if (G > 1) {
+      for (int p = 1; p < G; ++p) bnd[p] = 0;
+    }
+    const uint32_t lerr = read_err(ctx);   // overlap inside the local run
+    std::vector<uint64_t> mat((size_t)G * (G + 1));
+    {
+      std::vector<uint64_t> row(G + 1);
+      for (int p = 0; p < G; ++p) row[p] = bnd[p + 1] - bnd[p];
+      row[G] = lerr;
+      Small one(ctx, G + 1), all(ctx, (size_t)G * (G + 1));
+      one.put(row);
+      comm_ck(ctx, C.allgather(one.d, all.d, 8 * (G + 1), st), "all_gather counts");
+      mat = all.get((size_t)G * (G + 1));
+    }
+    std::vector<uint64_t> nrecv(G, 0);   // cells each rank receives
+    for (int src = 0; src < G; ++src) {
+      if (mat[(size_t)src * (G + 1) + G] & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
+      for (int dst = 0; dst < G; ++dst) nrecv[dst] += mat[(size_t)src * (G + 1) + dst];
+    }
+    for (int p = 0; p < G; ++p)
+      if (nrecv[p] == 0) fail(ctx, DVL_E_INVAL, "a rank would hold no cells (fewer distinct cells than ranks)");
+    for (int p = 0; p < r; ++p) cell_offset += nrecv[p];
+    const int64_t nr = (int64_t)nrecv[r];
+    if (nr >= (1ll << 30)) fail(ctx, DVL_E_RANGE, "a rank would hold >= 2^30 cells");
+
+    // ---- 4. exchange (codes, global ids, levels, member rows), each in curve order
+    const int64_t nr8 = (nr + 7) & ~7ll;
+    void* keys_r = dmalloc(ctx, (size_t)kb * nr);
+    unsigned long long* ids_r = dalloc<unsigned long long>(ctx, nr);
+    uint8_t* lev_r = dalloc<uint8_t>(ctx, nr8);
+    float* sc_r = dalloc<float>(ctx, (size_t)M * nr8);
+    tmp.push_back(keys_r);
+    tmp.push_back(ids_r);
+    tmp.push_back(lev_r);
+    tmp.push_back(sc_r);
+    std::vector<uint64_t> roff(G + 1, 0);   // received segment offsets (source rank order)
+    for (int p = 0; p < G; ++p) roff[p + 1] = roff[p] + mat[(size_t)p * (G + 1) + r];
+    auto exchange = [&](const void* sbase, void* rbase, size_t esize, const char* what) {
+      std::vector<const void*> sp(G);
+      std::vector<void*> rp(G);
+      std::vector<size_t> sb(G), rb(G);
+      for (int p = 0; p < G; ++p) {
+        sp[p] = static_cast<const char*>(sbase) + bnd[p] * esize;
+        sb[p] = (bnd[p + 1] - bnd[p]) * esize;
+        rp[p] = static_cast<char*>(rbase) + roff[p] * esize;
+        rb[p] = (roff[p + 1] - roff[p]) * esize;
+      }
+      comm_ck(ctx, C.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st), what);
+    };
+    exchange(skeys, keys_r, kb, "exchange codes");
+    exchange(ids_l, ids_r, 8, "exchange ids");
+    exchange(lev_l, lev_r, 1, "exchange levels");
+    for (int m = 0; m < M; ++m)
+      exchange(sc_l + (size_t)m * nl8, sc_r + (size_t)m * nr8, 4, "exchange scalars");
+
+    // ---- 5. combine the G sorted runs: the codes are distinct, so the bucket placement
+    //         (slots, offsets, bitmap rank) gives the order without re-encoding
+    CK(cudaMemsetAsync(ctx->d_err, 0, 4, st));
+    d.n = nr;
+    d.Lmax = lmax_global;
+    set_geometry(ctx, d);
+    Sorted fin = sort_codes(ctx, nullptr, nullptr, keys_r, nr, d.b, kb, tmp);
+    if (fin.keys == keys_r) tmp.erase(std::find(tmp.begin(), tmp.end(), keys_r));
+    d.keys = fin.keys;
+    d.perm = fin.perm;   // index into the received arrays (replaced by gids for get_sorted)
+    std::vector<const float*> rows(M);
+    for (int m = 0; m < M; ++m) rows[m] = sc_r + (size_t)m * nr8;
+    const float** d_rows = (const float**)dmalloc(ctx, sizeof(float*) * M);
+    tmp.push_back((void*)d_rows);
+    CK(cudaMemcpyAsync(d_rows, rows.data(), sizeof(float*) * M, cudaMemcpyHostToDevice, st));
+    IngestOut* d_rng = new_ingest(ctx, tmp);
+    gather_sorted(ctx, d, lev_r, d_rows, d_rng);
+    d.gids = dalloc<unsigned long long>(ctx, nr);
+    launch_gather_u64(ids_r, fin.perm, nr, d.gids, ctx->num_sms, st);
+    CKLAUNCH();
+
+    // ---- 6. overlap inside the range and across the rank boundaries; global ranges
+    const uint32_t ferr = read_err(ctx);
+    std::vector<uint64_t> ends(5, 0);
+    {
+      uint64_t k0 = 0, k1 = 0;
+      uint8_t l0 = 0, l1 = 0;
+      CK(cudaMemcpyAsync(&k0, d.keys, kb, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&k1, static_cast<char*>(d.keys) + (size_t)(nr - 1) * kb, kb,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&l0, d.level_s, 1, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&l1, d.level_s + nr - 1, 1, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ends = {ferr, k0, l0, k1, l1};
+    }
+    std::vector<uint64_t> allends;
+    {
+      Small one(ctx, 5), all(ctx, (size_t)G * 5);
+      one.put(ends);
+      comm_ck(ctx, C.allgather(one.d, all.d, 40, st), "all_gather run ends");
+      allends = all.get((size_t)G * 5);
+    }
+    for (int p = 0; p < G; ++p)
+      if (allends[5 * p] & kErrOverlap) fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells");
+    for (int p = 0; p + 1 < G; ++p) {
+      const uint64_t a = allends[5 * p + 3], La = allends[5 * p + 4];
+      const uint64_t b = allends[5 * (p + 1) + 1], Lb = allends[5 * (p + 1) + 2];
+      const uint64_t lena = 1ull << (3 * La), lenb = 1ull << (3 * Lb);
+      if (a >= b || (a & ~(lena - 1)) + lena > (b & ~(lenb - 1)))
+        fail(ctx, DVL_E_OVERLAP, "duplicate or overlapping cells across ranks");
+    }
+    {
+      IngestOut h;
+      read_ingest(ctx, d_rng, &h);
+      Small rng(ctx, 3 * (size_t)M);
+      std::vector<uint64_t> v(3 * (size_t)M);
+      for (int m = 0; m < M; ++m) {
+        v[m] = h.any[m] ? h.vmin[m] : 0xffffffffull;
+        v[M + m] = h.any[m] ? h.vmax[m] : 0ull;
+        v[2 * M + m] = h.any[m];
+      }
+      rng.put(v);
+      comm_ck(ctx, C.allreduce(rng.d, M, kU64, kMin, st), "all_reduce MIN ranges");
+      comm_ck(ctx, C.allreduce(rng.d + M, 2 * (size_t)M, kU64, kMax, st), "all_reduce MAX ranges");
+      v = rng.get(3 * (size_t)M);
+      for (int m = 0; m < M; ++m) {
+        h.vmin[m] = (uint32_t)v[m];
+        h.vmax[m] = (uint32_t)v[M + m];
+        h.any[m] = (uint32_t)v[2 * M + m];
+      }
+      ranges_from(d, h);
+    }
+    alloc_update_state(ctx, d);
+  } catch (Fail& f) {
+    cleanup();
+    free_dataset(ctx, d);
+    return f.s;
+  }
+  cleanup();
+  return commit_dataset(ctx, d, true, cell_offset, n_global, lmax_global);
+}
+
+}  // namespace
 
 dvl_status dvl_set_params(dvl_ctx* ctx, float P, float eps, dvl_maxv_mode mode) {
   if (!ctx) return DVL_E_INVAL;
@@ -1094,8 +1504,7 @@ static dvl_status sharded_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, d
       ctx->d_export = dalloc<int64_t>(ctx, (size_t)words);
       ctx->export_cap = words;
     }
-    if (const char* e = nccl_gather_totals(ctx->comm, (const uint64_t*)ctx->d_qtot,
-                                           (uint64_t*)ctx->d_totals, ctx->stream))
+    if (const char* e = ctx->comm->allgather(ctx->d_qtot, ctx->d_totals, 8, ctx->stream))
       fail(ctx, DVL_E_NCCL, std::string("all_gather of the totals: ") + e);
   } catch (Fail& f) {
     return f.s;
@@ -1104,8 +1513,7 @@ static dvl_status sharded_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, d
                                   ctx->comm_rank, ctx->d_export);
   if (s != DVL_OK) return s;
   const uint64_t MW = (uint64_t)ctx->ds.M * W;
-  if (const char* e = nccl_merge_export(ctx->comm, ctx->d_export, 2 * (W + MW), 3 * MW,
-                                        ctx->stream)) {
+  if (const char* e = ctx->comm->merge_export(ctx->d_export, 2 * (W + MW), 3 * MW, ctx->stream)) {
     set_err(ctx, std::string("merge of the exports: ") + e);
     return DVL_E_NCCL;
   }
@@ -1273,6 +1681,59 @@ dvl_status dvl_nccl_unique_id(void* id128) {
   return nccl_unique_id(id128) ? DVL_E_NCCL : DVL_OK;
 }
 
+dvl_status dvl_local_group_create(int nranks, void** group) {
+  if (!group || nranks < 1) return DVL_E_INVAL;
+  *group = new GroupHandle{local_group_create(nranks)};
+  return DVL_OK;
+}
+
+void dvl_local_group_destroy(void* group) {
+  if (!group) return;
+  GroupHandle* h = static_cast<GroupHandle*>(group);
+  local_group_release(h->g);
+  delete h;
+}
+
+dvl_status dvl_set_local_comm(dvl_ctx* ctx, void* group, int rank) {
+  if (!ctx) return DVL_E_INVAL;
+  GroupHandle* h = static_cast<GroupHandle*>(group);
+  if (!h || rank < 0 || rank >= local_group_size(h->g)) {
+    set_err(ctx, "bad local group or rank");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->comm) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      delete ctx->comm;
+      ctx->comm = nullptr;
+    }
+    attach_comm(ctx, make_local_comm(h->g, rank));
+  } catch (Fail& f) {
+    return f.s;
+  }
+  return DVL_OK;
+}
+
+dvl_status dvl_get_shard(dvl_ctx* ctx, dvl_shard_info* out) {
+  if (!ctx || !out) return DVL_E_INVAL;
+  if (!ctx->built) {
+    set_err(ctx, "no dataset");
+    return DVL_E_STATE;
+  }
+  memset(out, 0, sizeof *out);
+  out->cell_offset = ctx->cell_offset;
+  out->n_global = ctx->sharded ? ctx->n_global : (uint64_t)ctx->ds.n;
+  out->lmax_global = ctx->sharded ? ctx->lmax_global : ctx->ds.Lmax;
+  return DVL_OK;
+}
+
+dvl_status dvl_select_splitters(const uint64_t* samples, const uint64_t* counts, int nranks,
+                                int per_rank, uint64_t* splitters) {
+  if (!samples || !counts || !splitters || nranks < 2 || per_rank < 1) return DVL_E_INVAL;
+  return select_splitters(samples, counts, nranks, per_rank, splitters) ? DVL_OK : DVL_E_INVAL;
+}
+
 dvl_status dvl_set_comm(dvl_ctx* ctx, int nranks, int rank, const void* id128) {
   if (!ctx) return DVL_E_INVAL;
   if (nranks < 1 || rank < 0 || rank >= nranks || !id128) {
@@ -1283,17 +1744,13 @@ dvl_status dvl_set_comm(dvl_ctx* ctx, int nranks, int rank, const void* id128) {
     CK(cudaSetDevice(ctx->device));
     if (ctx->comm) {
       CK(cudaStreamSynchronize(ctx->stream));
-      nccl_comm_destroy(ctx->comm);
+      delete ctx->comm;
       ctx->comm = nullptr;
     }
-    void* c = nullptr;
-    if (const char* e = nccl_comm_init(&c, nranks, rank, id128))
-      fail(ctx, DVL_E_NCCL, std::string("ncclCommInitRank: ") + e);
-    dfree(ctx, ctx->d_totals);
-    ctx->d_totals = dalloc<unsigned long long>(ctx, (size_t)nranks);
-    ctx->comm = c;
-    ctx->comm_ranks = nranks;
-    ctx->comm_rank = rank;
+    const char* e = nullptr;
+    Comm* c = make_nccl_comm(nranks, rank, id128, &e);
+    if (!c) fail(ctx, DVL_E_NCCL, std::string("ncclCommInitRank: ") + (e ? e : "?"));
+    attach_comm(ctx, c);
   } catch (Fail& f) {
     return f.s;
   }
@@ -1446,8 +1903,11 @@ dvl_status dvl_get_sorted(dvl_ctx* ctx, uint64_t* codes, uint64_t* ids, dvl_mem 
       di = where == DVL_MEM_DEVICE ? ids : dalloc<uint64_t>(ctx, n);
       if (where != DVL_MEM_DEVICE) tmp.push_back(di);
     }
-    launch_widen(ctx->ds.keys, ctx->ds.key_bytes, ctx->ds.perm, n, dc, di, ctx->stream);
+    launch_widen(ctx->ds.keys, ctx->ds.key_bytes, ctx->ds.perm, n, dc, ctx->ds.gids ? nullptr : di,
+                 ctx->stream);
     CKLAUNCH();
+    if (ctx->ds.gids && di)   // distributed build: the global input ids
+      CK(cudaMemcpyAsync(di, ctx->ds.gids, 8 * n, cudaMemcpyDeviceToDevice, ctx->stream));
     if (where == DVL_MEM_HOST) {
       if (codes) CK(cudaMemcpyAsync(codes, dc, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
       if (ids) CK(cudaMemcpyAsync(ids, di, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));

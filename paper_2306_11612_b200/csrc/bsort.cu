@@ -20,6 +20,7 @@
 // the library uses the onesweep LSD sort (sort.cu).
 #include <algorithm>
 
+#include "bsort.cuh"
 #include "dvl_common.cuh"
 #include "dvl_internal.h"
 
@@ -122,6 +123,55 @@ scan_down_kernel(const uint32_t* __restrict__ cnt, int64_t nb, const uint32_t* _
     run += v[i];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) start[nb] = total;
+}
+
+// ---------------------------------------------------- slots of codes already computed
+// (the distributed build's received runs): the B1 counting step without the encode
+template <typename K, bool VEC>
+__global__ void __launch_bounds__(kBlock)
+bucket_slot_kernel(const K* __restrict__ keys, int64_t n, int lb, uint16_t* __restrict__ slot,
+                   uint32_t* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t groups = (n + 3) >> 2;
+  const int64_t wstride = (int64_t)gridDim.x * kBlock;
+  for (int64_t g0 = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); g0 < groups; g0 += wstride) {
+    const int64_t g = g0 + lane;
+    const int64_t h0 = g * 4;
+    const int cnt = g < groups ? (int)(n - h0 < 4 ? n - h0 : 4) : 0;
+    K code[4] = {0, 0, 0, 0};
+    if (VEC && cnt == 4) {
+      if (sizeof(K) == 4) {
+        const uint4 q = reinterpret_cast<const uint4*>(keys)[g];
+        code[0] = q.x; code[1] = q.y; code[2] = q.z; code[3] = q.w;
+      } else {
+        const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys) + 2 * g;
+        const ulonglong2 a = k2[0], c = k2[1];
+        code[0] = (K)a.x; code[1] = (K)a.y; code[2] = (K)c.x; code[3] = (K)c.y;
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) code[i] = keys[h0 + i];
+    }
+    uint32_t sl[4];
+    bucket_slots<K>(code, cnt, lb, count, sl);
+    if (cnt) store_slots(slot, g, h0, cnt, sl);
+  }
+}
+
+void launch_bucket_slot(const void* keys, int key_bytes, int64_t n, int lb, uint16_t* slot,
+                        uint32_t* count, int num_sms, cudaStream_t st) {
+  const int64_t groups = (n + 3) / 4;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + kBlock - 1) / kBlock,
+                                                                (int64_t)num_sms * 8));
+  const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(slot) & 7) == 0;
+  if (key_bytes == 4) {
+    if (vec) bucket_slot_kernel<uint32_t, true><<<grid, kBlock, 0, st>>>((const uint32_t*)keys, n, lb, slot, count);
+    else bucket_slot_kernel<uint32_t, false><<<grid, kBlock, 0, st>>>((const uint32_t*)keys, n, lb, slot, count);
+  } else {
+    using U = unsigned long long;
+    if (vec) bucket_slot_kernel<U, true><<<grid, kBlock, 0, st>>>((const U*)keys, n, lb, slot, count);
+    else bucket_slot_kernel<U, false><<<grid, kBlock, 0, st>>>((const U*)keys, n, lb, slot, count);
+  }
 }
 
 // ------------------------------------------------------------------- pass A: scatter

@@ -36,8 +36,13 @@ void launch_bucket_sort(const void* keys, const uint16_t* slot, int key_bytes, i
                         int64_t nb, const uint32_t* start, void* kA, uint32_t* vA, void* kB,
                         uint32_t* vB, uint32_t* work, uint32_t* err, int num_sms, cudaStream_t st);
 
+void launch_bucket_slot(const void* keys, int key_bytes, int64_t n, int lb, uint16_t* slot,
+                        uint32_t* count, int num_sms, cudaStream_t st);
+
 // sort.cu
 cudaError_t prepare_onesweep();
+void launch_key_hist(const void* keys, int key_bytes, int64_t n, int passes, uint32_t* hist,
+                     int num_sms, cudaStream_t st);
 void launch_hist_scan(const uint32_t* hist, uint32_t* base, int passes, cudaStream_t st);
 void launch_onesweep(const void* kin, const uint32_t* vin, void* kout, uint32_t* vout, int64_t n,
                      int key_bytes, int shift, const uint32_t* digit_base, uint32_t* status,
@@ -116,14 +121,42 @@ void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t
                    const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
                    const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
                    cudaStream_t st);
-// comm.cu: NCCL resolved at run time; each returns nullptr or an error text
+// dbuild.cu: the distributed build's device steps and splitter rule
+void launch_sample_keys(const void* keys, int key_bytes, int64_t n, int S, unsigned long long* out,
+                        cudaStream_t st);
+void launch_lower_bounds(const void* keys, int key_bytes, int64_t n, const unsigned long long* spl,
+                         int k, unsigned long long* out, cudaStream_t st);
+void launch_offset_ids(const uint32_t* perm, int64_t n, uint64_t off, unsigned long long* out,
+                       int num_sms, cudaStream_t st);
+void launch_gather_u64(const unsigned long long* src, const uint32_t* idx, int64_t n,
+                       unsigned long long* out, int num_sms, cudaStream_t st);
+bool select_splitters(const uint64_t* samples, const uint64_t* counts, int G, int S, uint64_t* out);
+
+// comm.cu: the collectives of sharded contexts (NCCL resolved at run time, or an
+// in-process group of contexts driven by host threads); each returns nullptr or an error text
+enum RedType { kU32 = 0, kU64 = 1, kI64 = 2 };
+enum RedOp { kSum = 0, kMin = 1, kMax = 2 };
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  // recv = nranks blocks of `bytes`, rank order
+  virtual const char* allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+  // in place, element-wise over the ranks
+  virtual const char* allreduce(void* buf, size_t count, RedType t, RedOp op, cudaStream_t st) = 0;
+  // in place: int64 MAX over [0, max_words), SUM over the next sum_words
+  virtual const char* merge_export(int64_t* buf, size_t max_words, size_t sum_words,
+                                   cudaStream_t st) = 0;
+  // send[p] (sbytes[p] bytes) to rank p, recv[p] (rbytes[p] bytes) from rank p
+  virtual const char* alltoallv(const void* const* send, const size_t* sbytes, void* const* recv,
+                                const size_t* rbytes, cudaStream_t st) = 0;
+};
+struct LocalGroup;
 const char* nccl_unique_id(void* id128);
-const char* nccl_comm_init(void** comm, int nranks, int rank, const void* id128);
-void nccl_comm_destroy(void* comm);
-const char* nccl_gather_totals(void* comm, const uint64_t* total, uint64_t* totals,
-                               cudaStream_t st);
-const char* nccl_merge_export(void* comm, int64_t* buf, size_t max_words, size_t sum_words,
-                              cudaStream_t st);
+Comm* make_nccl_comm(int nranks, int rank, const void* id128, const char** err);
+LocalGroup* local_group_create(int n);
+void local_group_release(LocalGroup* g);
+int local_group_size(const LocalGroup* g);
+Comm* make_local_comm(LocalGroup* g, int rank);
 size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);
 cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds

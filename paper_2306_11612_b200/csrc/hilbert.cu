@@ -17,6 +17,7 @@
 #include <map>
 #include <vector>
 
+#include "bsort.cuh"
 #include "dvl_common.cuh"
 #include "dvl_internal.h"
 
@@ -203,7 +204,6 @@ encode_bucket_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restri
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
   const int64_t groups = (n + 3) >> 2;
   const int64_t wstride = (int64_t)gridDim.x * (kBlock / 32) * 32;
   for (int64_t g0 = ((int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5)) * 32; g0 < groups;
@@ -253,37 +253,9 @@ encode_bucket_kernel(const uint32_t* __restrict__ lower, const uint8_t* __restri
     } else {
       for (int i = 0; i < cnt; ++i) keys[h0 + i] = code[i];
     }
-    const uint32_t b0 = cnt ? (uint32_t)(code[0] >> lb) : 0xffffffffu;
-    const bool same = cnt == 4 && (uint32_t)(code[1] >> lb) == b0 && (uint32_t)(code[2] >> lb) == b0 &&
-                      (uint32_t)(code[3] >> lb) == b0;
     uint32_t sl[4];
-    if (__all_sync(0xffffffffu, same || cnt == 0)) {   // every lane's four cells share a bucket
-      const uint32_t peers = __match_any_sync(0xffffffffu, b0);
-      uint32_t base = 0;
-      if (b0 != 0xffffffffu && (peers & lt) == 0) base = atomicAdd(count + b0, 4u * __popc(peers));
-      base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1) + 4u * __popc(peers & lt);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) sl[i] = base + i;
-    } else {
-      uint32_t bkt[4], peers[4], base[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        bkt[i] = i < cnt ? (uint32_t)(code[i] >> lb) : 0xffffffffu;
-        peers[i] = __match_any_sync(0xffffffffu, bkt[i]);
-        base[i] = 0;
-        if (bkt[i] != 0xffffffffu && (peers[i] & lt) == 0)
-          base[i] = atomicAdd(count + bkt[i], (uint32_t)__popc(peers[i]));
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        sl[i] = __shfl_sync(0xffffffffu, base[i], __ffs(peers[i]) - 1) + __popc(peers[i] & lt);
-    }
-    if (cnt == 4) {
-      reinterpret_cast<uint2*>(slot)[g] = make_uint2((sl[0] & 0xffffu) | (sl[1] << 16),
-                                                     (sl[2] & 0xffffu) | (sl[3] << 16));
-    } else {
-      for (int i = 0; i < cnt; ++i) slot[h0 + i] = (uint16_t)sl[i];
-    }
+    bucket_slots<K>(code, cnt, lb, count, sl);
+    store_slots(slot, g, h0, cnt, sl);
   }
 }
 

@@ -180,6 +180,34 @@ onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
   }
 }
 
+// the digit histograms of all passes over codes already computed (the LSD sort of the
+// distributed build's received runs; B1 builds them while it encodes)
+template <typename K>
+__global__ void __launch_bounds__(kBlock)
+key_hist_kernel(const K* __restrict__ keys, int64_t n, int passes, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_hist[8][256];
+  for (int i = threadIdx.x; i < passes * 256; i += kBlock) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t h = (int64_t)blockIdx.x * kBlock + threadIdx.x; h < n; h += (int64_t)gridDim.x * kBlock) {
+    const uint64_t code = keys[h];
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(code >> (8 * p)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kBlock) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+void launch_key_hist(const void* keys, int key_bytes, int64_t n, int passes, uint32_t* hist,
+                     int num_sms, cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, (int64_t)num_sms * 8));
+  if (key_bytes == 4)
+    key_hist_kernel<uint32_t><<<grid, kBlock, 0, st>>>((const uint32_t*)keys, n, passes, hist);
+  else
+    key_hist_kernel<unsigned long long><<<grid, kBlock, 0, st>>>((const unsigned long long*)keys, n, passes, hist);
+}
+
 void launch_hist_scan(const uint32_t* hist, uint32_t* base, int passes, cudaStream_t st) {
   hist_scan_kernel<<<passes, 256, 0, st>>>(hist, base);
 }

@@ -34,7 +34,9 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_hilbert_encode_host", "dvl_hilbert_states", "dvl_set_global_bits",
            "dvl_set_shard", "dvl_shard_total", "dvl_shard_export_words", "dvl_shard_reduce",
            "dvl_shard_finish", "dvl_set_timing", "dvl_locate", "dvl_set_level_scale",
-           "dvl_nccl_unique_id", "dvl_set_comm"]
+           "dvl_nccl_unique_id", "dvl_set_comm", "dvl_local_group_create",
+           "dvl_local_group_destroy", "dvl_set_local_comm", "dvl_get_shard",
+           "dvl_select_splitters"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -117,6 +119,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_set_level_scale": (i32, [P, i32]),
         "dvl_nccl_unique_id": (i32, [P]),
         "dvl_set_comm": (i32, [P, i32, i32, P]),
+        "dvl_local_group_create": (i32, [i32, ctypes.POINTER(ctypes.c_void_p)]),
+        "dvl_local_group_destroy": (None, [P]),
+        "dvl_set_local_comm": (i32, [P, P, i32]),
+        "dvl_get_shard": (i32, [P, ctypes.POINTER(_ShardInfo)]),
+        "dvl_select_splitters": (i32, [P, P, i32, i32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -300,6 +307,9 @@ class Context:
                                  DEVICE if dev else HOST)
         self._check(st, "dvl_build")
         self.M, self.n = M, n
+        if getattr(self, "_group", None) is not None or getattr(self, "_comm", False):
+            # distributed build: this context now holds its range of the curve order
+            self.n = int(self.info()["n"])
 
     def set_level_scale(self, scale: str = "width"):
         """Eq. 3's level factor: "width" (2^L, default) or "volume" (2^3L)."""
@@ -424,6 +434,20 @@ class Context:
         """Join the context's own NCCL communicator (collective over the ranks)."""
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         self._check(self._lib.dvl_set_comm(self._h, nranks, rank, buf), "dvl_set_comm")
+        self._comm = True
+
+    def set_local_comm(self, group: "LocalGroup", rank: int):
+        """Join an in-process group of contexts as `rank` (see LocalGroup)."""
+        self._group = group   # keep the handle alive with the context
+        self._check(self._lib.dvl_set_local_comm(self._h, group._h, rank), "dvl_set_local_comm")
+
+    def shard(self) -> dict:
+        """This context's place in the global curve order: cell_offset, n_global,
+        lmax_global (a single-context build: offset 0 and its own n)."""
+        info = _ShardInfo()
+        self._check(self._lib.dvl_get_shard(self._h, ctypes.byref(info)), "dvl_get_shard")
+        return {"cell_offset": info.cell_offset, "n_global": info.n_global,
+                "lmax_global": info.lmax_global}
 
     def set_global_bits(self, bits: int):
         self._check(self._lib.dvl_set_global_bits(self._h, bits), "dvl_set_global_bits")
@@ -488,3 +512,40 @@ def nccl_unique_id() -> bytes:
     if load().dvl_nccl_unique_id(buf) != 0:
         raise DvlError("dvl_nccl_unique_id: libnccl.so.2 not available")
     return buf.raw
+
+
+class LocalGroup:
+    """An in-process group of `nranks` contexts (one host thread per rank), the ABI's
+    stand-in for an NCCL communicator on a single GPU: with it every context's build is the
+    distributed sample sort and its get_polylines the sharded edit, all inside the library
+    (dvl_local_group_create / dvl_set_local_comm)."""
+
+    def __init__(self, nranks: int):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        st = self._lib.dvl_local_group_create(nranks, ctypes.byref(h))
+        if st:
+            raise DvlError(st, "dvl_local_group_create")
+        self._h, self.nranks = h, nranks
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                self._lib.dvl_local_group_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def select_splitters(samples, counts, per_rank: int) -> np.ndarray:
+    """The library's sample-sort splitter rule on the host (dvl_select_splitters): samples is
+    (G, per_rank) u64 (rank p's first min(per_rank, counts[p]) entries are its regular samples),
+    counts the cells per rank; returns G-1 strictly increasing splitters."""
+    samples = np.ascontiguousarray(samples, np.uint64)
+    counts = np.ascontiguousarray(counts, np.uint64)
+    G = len(counts)
+    out = np.empty(max(G - 1, 1), np.uint64)
+    st = load().dvl_select_splitters(_ptr(samples), _ptr(counts), G, per_rank, _ptr(out))
+    if st:
+        raise DvlError(st, "dvl_select_splitters")
+    return out[: G - 1]

@@ -1,10 +1,12 @@
-"""Distributed build + sharded TF update through the C ABI on one GPU: G ranks as G threads
-(paper_2306_11612_b200.dist_build.ThreadCollectives), each with its own dvl context and a
-round-robin slice of the input order.  After the sample sort each context must hold one
-contiguous piece of the global curve order (the union equals a one-context build: codes,
-levels, scalars), and the sharded polylines must equal the one-context polylines (bit for
-bit on counts, min/max and bin ranges) and the oracle.  (NCCL cannot put two ranks on one
-GPU; the same function runs over torch.distributed in bench.py under torchrun.)
+"""The distributed build and the sharded TF update through the C ABI on one GPU: G contexts in
+an in-process group (dvl.LocalGroup, driven by G host threads: the library's stand-in for an
+NCCL communicator, same code above the transport), each given a slice of the input order --
+round robin, or uneven with an empty rank.  dvl_build runs the whole Hilbert-key sample
+sort in the library (SURVEY 8(e) "Build"); afterwards each context must hold one contiguous
+piece of the global curve order whose union equals the oracle's one-process build (codes,
+input ids, levels, scalars), and get_polylines -- the sharded edit with both exchanges in
+the library -- must equal the oracle and a one-context run, over a run of edits of one
+member (edit-cache mode).
 """
 import threading
 
@@ -13,6 +15,8 @@ import pytest
 
 from oracle import oracle as o
 import synth
+
+from tests.test_gpu_parity import check_update, octree
 
 pytestmark = pytest.mark.gpu
 
@@ -24,23 +28,13 @@ def dvl():
     return m
 
 
-def octree(E, Lmax, seed, p=0.45):
-    rng = np.random.default_rng(seed)
-    lower, level = synth.uniform_cells(E >> Lmax)
-    lower = (lower << np.uint32(Lmax)).astype(np.uint32)
-    level = np.full(len(level), Lmax, np.uint8)
-    for L in range(Lmax, 0, -1):
-        mask = (level == L) & (rng.random(len(level)) < p)
-        lower, level = synth.refine(lower, level, mask)
-    return lower, level
-
-
 def run_threads(fns):
     errs = [None] * len(fns)
+    outs = [None] * len(fns)
 
     def wrap(i):
         try:
-            fns[i]()
+            outs[i] = fns[i]()
         except BaseException as e:   # noqa: BLE001
             errs[i] = e
 
@@ -49,75 +43,119 @@ def run_threads(fns):
         t.start()
     for t in ts:
         t.join(timeout=600)
+    return outs, errs
+
+
+def slices(n, G, kind, rng):
+    if kind == "round_robin":
+        return [np.arange(r, n, G) for r in range(G)]
+    perm = rng.permutation(n)
+    cuts = [0, 0] + sorted(rng.choice(np.arange(1, n), G - 2, replace=False).tolist()) + [n]
+    if G == 2:
+        cuts = [0, 0, n]
+    return [np.sort(perm[cuts[r]:cuts[r + 1]]) for r in range(G)]   # rank 0 holds nothing
+
+
+def build_group(dvl, G, lower, level, scal, parts, **kw):
+    grp = dvl.LocalGroup(G)
+    ctxs = [dvl.Context(device=0, **kw) for _ in range(G)]
+    for r, c in enumerate(ctxs):
+        c.set_local_comm(grp, r)
+    _, errs = run_threads([lambda r=r: ctxs[r].build(lower[parts[r]], level[parts[r]],
+                                                      np.ascontiguousarray(scal[:, parts[r]]))
+                           for r in range(G)])
+    return ctxs, errs
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("kind", ["round_robin", "uneven"])
+def test_library_distributed_build_and_sharded_edits(dvl, G, kind):
+    lower, level = octree(64, 3, 20 + G)
+    n, M, W = len(level), 4, 300
+    rng = np.random.default_rng(G)
+    scal = rng.standard_normal((M, n)).astype(np.float32)
+    parts = slices(n, G, kind, rng)
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts)
     for e in errs:
         if e is not None:
             raise e
-
-
-@pytest.mark.parametrize("G", [2, 3])
-def test_distributed_build_and_sharded_update(dvl, G):
-    import torch
-    from paper_2306_11612_b200 import dist_build as db, shard
-    lower, level = octree(64, 3, 20 + G)
-    M = 4
-    rng = np.random.default_rng(G)
-    scal = rng.standard_normal((M, len(level))).astype(np.float32)
-    tfs = np.stack([synth.random_tf(70 + m, 256, member=m) for m in range(M)])
-    W = 300
-    ctxs = [dvl.Context(device=0) for _ in range(G)]
-    colls = db.ThreadCollectives.group(G)
-    infos = [None] * G
-
-    def rank_fn(r):
-        def f():
-            idx = np.arange(r, len(level), G)
-            lo = torch.from_numpy(lower[idx].astype(np.int32)).cuda()
-            lv = torch.from_numpy(level[idx]).cuda()
-            sc = torch.from_numpy(np.ascontiguousarray(scal[:, idx])).cuda()
-            infos[r] = db.distributed_build(ctxs[r], lo, lv, sc, colls[r], samples=128)
-        return f
-
-    run_threads([rank_fn(r) for r in range(G)])
     B = o.build(lower, level, scal)
-    codes = np.concatenate([c.get_sorted()[0] for c in ctxs])
-    assert np.array_equal(codes, B.codes)
+    order = np.concatenate(parts)            # global input id -> input index
+    srt = [c.get_sorted() for c in ctxs]
+    assert np.array_equal(np.concatenate([s[0] for s in srt]), B.codes)
+    assert np.array_equal(order[np.concatenate([s[1] for s in srt]).astype(np.int64)], B.perm.astype(np.int64))
     data = [c.get_sorted_data() for c in ctxs]
     assert np.array_equal(np.concatenate([d[0] for d in data]), B.level_s)
-    assert np.array_equal(np.concatenate([d[1] for d in data], axis=1), B.scal_s)
-    assert [i["offset"] for i in infos] == list(np.cumsum([0] + [i["n_local"] for i in infos])[:-1])
-    assert all(min(i["sent"]) > 0 for i in infos)
-    # sharded update with the two exchanges done by torch ops (as in test_gpu_shard)
-    for c in ctxs:
-        for m in range(M):
-            c.update_tf(m, tfs[m])
-    totals = torch.zeros(G, dtype=torch.int64, device="cuda")
-    for g, c in enumerate(ctxs):
-        c.shard_total(totals[g:g + 1])
-    torch.cuda.synchronize()
-    exports = []
-    for g, c in enumerate(ctxs):
-        buf = torch.empty(c.shard_export_words(W), dtype=torch.int64, device="cuda")
-        c.shard_reduce(W, totals, g, buf)
-        exports.append(buf)
-    torch.cuda.synchronize()
-    planes = [shard.split_planes(e, W, M) for e in exports]
-    merged = torch.cat([torch.stack([p[0] for p in planes]).max(0).values,
-                        torch.stack([p[1] for p in planes]).max(0).values,
-                        torch.stack([p[2] for p in planes]).sum(0)])
-    out = ctxs[0].shard_finish(W, merged)
-    U = o.update(B, tfs, W)
-    assert int(totals.sum().item()) == U.Qtot
-    ref = U.vertices
-    for k in ("count", "t_min", "t_max"):
-        assert np.array_equal(out[k], ref[k])
-    rel = np.abs(out["t_mean"].astype(np.float64) - ref["t_mean"]) / np.maximum(ref["t_mean"], 1e-30)
-    assert rel.max() <= 1e-5
+    assert np.array_equal(np.concatenate([d[1] for d in data], axis=1).view(np.uint32), B.scal_s.view(np.uint32))
+    shards = [c.shard() for c in ctxs]
+    sizes = [len(s[0]) for s in srt]
+    assert [s["cell_offset"] for s in shards] == np.cumsum([0] + sizes)[:-1].tolist()
+    assert all(s["n_global"] == n and s["lmax_global"] == B.Lmax for s in shards)
+    assert min(sizes) > 0
+    # sharded edits: every rank's get_polylines runs both exchanges in the library
+    tfs = np.stack([synth.random_tf(70 + m, 256, member=m) for m in range(M)])
     one = dvl.Context(device=0)
     one.build(lower, level, scal)
     for m in range(M):
         one.update_tf(m, tfs[m])
-    single = one.get_polylines(W)
-    for k in ("count", "t_min", "t_max"):
-        assert np.array_equal(single[k], out[k])
+        for c in ctxs:
+            c.update_tf(m, tfs[m])
+    for e in range(3):
+        if e:
+            tfs[0] = synth.tf_edit(5, e)
+            one.update_tf(0, tfs[0])
+            for c in ctxs:
+                c.update_tf(0, tfs[0])
+        outs, errs = run_threads([lambda c=c: c.get_polylines(W) for c in ctxs])
+        for err in errs:
+            if err is not None:
+                raise err
+        U = o.update(B, tfs, W)
+        single = one.get_polylines(W)
+        for out in outs:
+            assert np.array_equal(out.view(np.uint8), outs[0].view(np.uint8))
+            for k in ("count", "t_min", "t_max"):
+                assert np.array_equal(out[k], U.vertices[k]) and np.array_equal(out[k], single[k])
+            rel = np.abs(out["t_mean"].astype(np.float64) - U.vertices["t_mean"]) / np.maximum(U.vertices["t_mean"], 1e-30)
+            assert rel.max() <= 1e-5
+        # each shard's prefix of its own cells (shard-relative) plus the earlier shards' total
+        # is the global Q (Eq. 4)
+        for c, sh in zip(ctxs, shards):
+            off = sh["cell_offset"]
+            q = c.get_prefix().astype(object) + (int(U.Q[off - 1]) if off else 0)
+            assert np.array_equal(q.astype(np.uint64), U.Q[off:off + len(q)])
     for c in ctxs + [one]:
+        c.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_overlap_across_ranks_fails_everywhere(dvl, G):
+    """A duplicate cell held by two different ranks: every rank returns DVL_E_OVERLAP."""
+    lower, level = octree(32, 2, 7)
+    n = len(level)
+    scal = np.random.default_rng(1).standard_normal((2, n)).astype(np.float32)
+    parts = [np.arange(r, n, G) for r in range(G)]
+    parts[1] = np.concatenate([parts[1], parts[0][:1]])     # rank 1 repeats a cell of rank 0
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts)
+    assert all(e is not None and getattr(e, "status", "") == "DVL_E_OVERLAP" for e in errs), errs
+    for c in ctxs:
+        c.close()
+
+
+def test_u64_keys_and_lsd_combine(dvl):
+    """3b > 36 (E = 2^13): the received runs are combined by the onesweep LSD sort."""
+    from tests.test_gpu_parity import sparse_cells
+    lower, level = sparse_cells(1 << 13, 20000, 3, Lmax=4)
+    n = len(level)
+    scal = np.random.default_rng(2).standard_normal((3, n)).astype(np.float32)
+    G = 3
+    parts = [np.arange(r, n, G) for r in range(G)]
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts)
+    for e in errs:
+        if e is not None:
+            raise e
+    B = o.build(lower, level, scal)
+    assert B.b == 13
+    assert np.array_equal(np.concatenate([c.get_sorted()[0] for c in ctxs]), B.codes)
+    for c in ctxs:
         c.close()
