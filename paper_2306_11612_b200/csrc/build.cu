@@ -161,6 +161,15 @@ gather_validate8_kernel(const K* __restrict__ keys, const uint32_t* __restrict__
         key[i] = i < cnt ? keys[k0 + i] : (K)0;
       }
     }
+    // a source index out of range can only come from duplicate codes (the sort's slots
+    // of a duplicate are not all written): the cell is skipped and the build fails OVERLAP
+#pragma unroll
+    for (int i = 0; i < kGI; ++i) {
+      if (i < cnt && p[i] >= (uint64_t)n) {
+        bad = 1;
+        p[i] = 0;
+      }
+    }
     uint32_t L[kGI];
 #pragma unroll
     for (int i = 0; i < kGI; ++i) L[i] = i < cnt ? (uint32_t)level_in[p[i]] : 0u;
@@ -169,7 +178,8 @@ gather_validate8_kernel(const K* __restrict__ keys, const uint32_t* __restrict__
     uint32_t Lnext = __shfl_down_sync(0xffffffffu, L[0], 1);
     if (lane == 31 && cnt == kGI && k0 + kGI < n) {
       knext = keys[k0 + kGI];
-      Lnext = level_in[perm[k0 + kGI]];
+      const uint32_t pn = perm[k0 + kGI];
+      Lnext = pn < (uint64_t)n ? level_in[pn] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kGI; ++i) {

@@ -50,8 +50,10 @@ __global__ void gather_u64_kernel(const unsigned long long* __restrict__ src,
                                   const uint32_t* __restrict__ idx, int64_t n,
                                   unsigned long long* __restrict__ out) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    out[k] = src[idx[k]];
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = idx[k];
+    out[k] = i < n ? src[i] : 0ull;   // out of range only with duplicate codes (OVERLAP)
+  }
 }
 
 static int grid_for(int64_t n, int num_sms) {
