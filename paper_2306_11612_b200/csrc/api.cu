@@ -44,6 +44,13 @@ struct Dataset {
   TmaPlan plan{};
   int grid = 0;                           // pass-2 chunks = CTAs
   int grid1 = 0;                          // pass-1 chunks = CTAs (look-back granularity)
+  // edit-cache pass 1 at M > 8: its stage holds 13 B per cell, not 4M + 1, so it runs as
+  // several CTAs per SM (as many consumer warps per SM as the M <= 4 configuration), with
+  // its own chunks; pass 2 takes the chunking of the pass 1 that ran last
+  TmaPlan plan_c{};
+  int grid1_c = 0;
+  bool plan_c_ok = false;
+  bool last_c = false;
   int planN = 0;                          // TF size the plan was made for
   int chunk_cap = 0;
   unsigned long long* chunk_status = nullptr;   // grid + 1 (last slot: chunk counter)
@@ -382,22 +389,46 @@ void ensure_plan(dvl_ctx* ctx) {
   int G1 = std::min(pl.tiles1, ctx->num_sms * bps1);
   pl.tpc1 = (pl.tiles1 + G1 - 1) / G1;
   G1 = (pl.tiles1 + pl.tpc1 - 1) / pl.tpc1;
-  if (G1 + 1 > d.chunk_cap) {
-    unsigned long long* cs = dalloc<unsigned long long>(ctx, G1 + 1);
-    unsigned long long* cp = dalloc<unsigned long long>(ctx, G1);
+  // the edit-cache plan (M > 8): 3 CTAs per SM, stages of 13 B per cell, the TF table read
+  // through L1 (the edited member's only)
+  TmaPlan pc = pl;
+  int G1c = 0;
+  bool pc_ok = false;
+  if (d.M > 8 && d.M >= 3) {
+    pc.tab_bytes = 0;
+    pc.stage_bytes1 = round128((size_t)T1 * 13);
+    pc.stages1 = fit(third, 0, pc.stage_bytes1);
+    if (pc.stages1 >= 2 && tma_blocks_per_sm_cache(d.M, pc) >= 3) {
+      G1c = std::min(pl.tiles1, ctx->num_sms * 3);
+      pc.tpc1 = (pl.tiles1 + G1c - 1) / G1c;
+      G1c = (pl.tiles1 + pc.tpc1 - 1) / pc.tpc1;
+      pc_ok = true;
+    }
+  }
+  const int cap = std::max(G1, G1c) + 1;   // chunk status words + the chunk counters' word
+  if (cap > d.chunk_cap) {
+    unsigned long long* cs = dalloc<unsigned long long>(ctx, cap);
+    unsigned long long* cp = dalloc<unsigned long long>(ctx, cap);
     // the last word holds pass 1's self-resetting chunk counters: zero once here
-    CK(cudaMemsetAsync(cs, 0, sizeof(unsigned long long) * (G1 + 1), ctx->stream));
+    CK(cudaMemsetAsync(cs, 0, sizeof(unsigned long long) * cap, ctx->stream));
     dfree(ctx, d.chunk_status);
     dfree(ctx, d.chunk_prefix);
     d.chunk_status = cs;
     d.chunk_prefix = cp;
-    d.chunk_cap = G1 + 1;
+    d.chunk_cap = cap;
   }
   d.plan = pl;
+  d.plan_c = pc;
+  d.plan_c_ok = pc_ok;
+  d.grid1_c = G1c;
+  d.last_c = false;
   d.grid = G;
   d.grid1 = G1;
   d.planN = ctx->N;
 }
+
+// the pass-1 chunking pass 2 must use: that of the last pass 1
+const TmaPlan& pass2_plan(const Dataset& d) { return d.last_c ? d.plan_c : d.plan; }
 
 // U0-U2: (member >= 0: install the staged TF of that member), maxV, pass 1 (weights +
 // decoupled look-back scan).
@@ -409,7 +440,7 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   tic(ctx, PH_MAXV);
   const bool exact = ctx->mode == DVL_MAXV_EXACT;
   launch_prologue(ctx, member, exact ? -1 : ctx->mode, d.tma ? d.chunk_status : nullptr,
-                  d.tma ? d.grid1 : 0);
+                  d.tma ? d.chunk_cap - 1 : 0);
   if (exact) {
     // 4 cells per thread on the TMA layout (tiles of 4 * 256 * k cells), else the tile's
     const int per = d.tma ? 4 : d.items;
@@ -445,9 +476,14 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
   }
   tic(ctx, PH_WSCAN);
   if (d.tma) {
-    launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid1, d.chunk_status,
-                              reinterpret_cast<uint32_t*>(d.chunk_status + d.grid1), d.chunk_prefix,
-                              ctx->d_qtot, d.tile_meta, d.meta2, cmode, ctx->stream);
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(d.chunk_status + d.chunk_cap - 1);
+    d.last_c = cmode == 1 && d.plan_c_ok;
+    if (d.last_c)
+      launch_weights_reduce_tma(false, p, d.plan_c, d.grid1_c, d.chunk_status, ctr, d.chunk_prefix,
+                                ctx->d_qtot, d.tile_meta, d.meta2, cmode, ctx->stream);
+    else
+      launch_weights_reduce_tma(d.plan.tab_bytes > 0, p, d.plan, d.grid1, d.chunk_status, ctr,
+                                d.chunk_prefix, ctx->d_qtot, d.tile_meta, d.meta2, cmode, ctx->stream);
     CKLAUNCH();
     if (export_q) {
       launch_q_export_tma(false, p, d.plan, d.grid, d.chunk_prefix, ctx->d_qtot, ctx->d_err, q_out,
@@ -1542,7 +1578,7 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
+      launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
                         ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
                           ctx->num_sms, ctx->stream);
     else
@@ -1793,7 +1829,7 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
     if (d.tma)
-      launch_agg_reduce(p, d.plan, d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
+      launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
                         ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
                           ctx->num_sms, ctx->stream);
     else

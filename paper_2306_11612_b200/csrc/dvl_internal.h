@@ -108,6 +108,7 @@ int tma_items_for(int M);
 size_t tma_smem(const TmaPlan& plan);
 cudaError_t debug_stats(unsigned long long* out8, bool reset);
 int tma_blocks_per_sm(int M, bool smem_tab, const TmaPlan& plan, int pass);
+int tma_blocks_per_sm_cache(int M, const TmaPlan& plan);
 int tma_tile2_cells(int M);
 int tma_pass2_ctas_per_sm(int M);
 int tma_warp_tile_cells();
