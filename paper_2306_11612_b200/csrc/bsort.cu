@@ -178,62 +178,82 @@ void launch_bucket_slot(const void* keys, int key_bytes, int64_t n, int lb, uint
 // every cell to start[bucket] + its slot from B1: a streaming pass with no atomics (a slot
 // past the bucket's end -- only possible with more than 65536 duplicate codes -- is an
 // overlap and is dropped)
+constexpr int kScatGP = 2;   // groups of 4 cells per lane and iteration (8 cells)
+
 template <typename K, bool VEC>
 __global__ void __launch_bounds__(kBlock)
 bucket_scatter_kernel(const K* __restrict__ keys, const uint16_t* __restrict__ slot, int64_t n,
                       int lb, const uint32_t* __restrict__ start, K* __restrict__ kout,
                       uint32_t* __restrict__ vout, uint32_t* err) {
-  // the warp's 128 destinations are staged in shared memory and stored transposed (lane l
-  // writes cells l, l + 32, ...): consecutive cells mostly go to consecutive slots, so each
-  // store instruction writes a few whole sectors instead of 32 scattered pieces
-  __shared__ K s_k[kBlock / 32][128];
-  __shared__ uint32_t s_p[kBlock / 32][128];
+  // each lane takes kScatGP groups of 4 cells per iteration (all their loads issued before
+  // the bucket-start lookups, all those before the stores); the warp's destinations are
+  // staged in shared memory and stored transposed (lane l writes cells l, l + 32, ...):
+  // consecutive cells mostly go to consecutive slots, so each store instruction writes a
+  // few whole sectors instead of 32 scattered pieces
+  constexpr int WC = 128 * kScatGP;   // cells per warp and iteration
+  __shared__ K s_k[kBlock / 32][WC];
+  __shared__ uint32_t s_p[kBlock / 32][WC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t groups = (n + 3) >> 2;
   bool bad = false;
-  for (int64_t g0 = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); g0 < groups;
-       g0 += (int64_t)gridDim.x * kBlock) {
-    const int64_t g = g0 + lane;
-    const int64_t h0 = g * 4;
-    const int cnt = g < groups ? (int)(n - h0 < 4 ? n - h0 : 4) : 0;
-    K code[4] = {0, 0, 0, 0};
-    uint32_t sl[4] = {0, 0, 0, 0};
-    if (g >= groups) {
-    } else if (VEC && cnt == 4) {
-      if (sizeof(K) == 4) {
-        const uint4 q = reinterpret_cast<const uint4*>(keys)[g];
-        code[0] = q.x; code[1] = q.y; code[2] = q.z; code[3] = q.w;
+  for (int64_t g0 = ((int64_t)blockIdx.x * (kBlock / 32) + warp) * (32 * kScatGP); g0 < groups;
+       g0 += (int64_t)gridDim.x * (kBlock / 32) * (32 * kScatGP)) {
+    K code[kScatGP][4];
+    uint32_t sl[kScatGP][4];
+    int cnt[kScatGP];
+#pragma unroll
+    for (int j = 0; j < kScatGP; ++j) {
+      const int64_t g = g0 + 32 * j + lane;
+      const int64_t h0 = g * 4;
+      cnt[j] = g < groups ? (int)(n - h0 < 4 ? n - h0 : 4) : 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        code[j][i] = 0;
+        sl[j][i] = 0;
+      }
+      if (VEC && cnt[j] == 4) {
+        if (sizeof(K) == 4) {
+          const uint4 q = reinterpret_cast<const uint4*>(keys)[g];
+          code[j][0] = q.x; code[j][1] = q.y; code[j][2] = q.z; code[j][3] = q.w;
+        } else {
+          const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys) + 2 * g;
+          const ulonglong2 a = k2[0], c = k2[1];
+          code[j][0] = (K)a.x; code[j][1] = (K)a.y; code[j][2] = (K)c.x; code[j][3] = (K)c.y;
+        }
+        const uint2 s2 = reinterpret_cast<const uint2*>(slot)[g];
+        sl[j][0] = s2.x & 0xffffu; sl[j][1] = s2.x >> 16; sl[j][2] = s2.y & 0xffffu; sl[j][3] = s2.y >> 16;
       } else {
-        const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys) + 2 * g;
-        const ulonglong2 a = k2[0], c = k2[1];
-        code[0] = (K)a.x; code[1] = (K)a.y; code[2] = (K)c.x; code[3] = (K)c.y;
-      }
-      const uint2 s2 = reinterpret_cast<const uint2*>(slot)[g];
-      sl[0] = s2.x & 0xffffu; sl[1] = s2.x >> 16; sl[2] = s2.y & 0xffffu; sl[3] = s2.y >> 16;
-    } else {
-      for (int i = 0; i < cnt; ++i) {
-        code[i] = keys[h0 + i];
-        sl[i] = slot[h0 + i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < cnt[j]) {
+            code[j][i] = keys[h0 + i];
+            sl[j][i] = slot[h0 + i];
+          }
+        }
       }
     }
-    uint32_t pos[4], lim[4];
+    uint32_t pos[kScatGP][4], lim[kScatGP][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t bkt = (uint32_t)(code[i] >> lb);
-      pos[i] = i < cnt ? start[bkt] + sl[i] : 0u;
-      lim[i] = i < cnt ? start[bkt + 1] : 0u;
-    }
+    for (int j = 0; j < kScatGP; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool ok = i < cnt && pos[i] < lim[i];
-      bad |= i < cnt && !ok;
-      s_k[warp][4 * lane + i] = code[i];
-      s_p[warp][4 * lane + i] = ok ? pos[i] : 0xffffffffu;
-    }
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t bkt = (uint32_t)(code[j][i] >> lb);
+        pos[j][i] = i < cnt[j] ? start[bkt] + sl[j][i] : 0u;
+        lim[j][i] = i < cnt[j] ? start[bkt + 1] : 0u;
+      }
+#pragma unroll
+    for (int j = 0; j < kScatGP; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = i < cnt[j] && pos[j][i] < lim[j][i];
+        bad |= i < cnt[j] && !ok;
+        s_k[warp][128 * j + 4 * lane + i] = code[j][i];
+        s_p[warp][128 * j + 4 * lane + i] = ok ? pos[j][i] : 0xffffffffu;
+      }
     __syncwarp();
     const int64_t c0 = 4 * g0;   // the warp's first cell
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 4 * kScatGP; ++i) {
       const int c = 32 * i + lane;
       const uint32_t ps = s_p[warp][c];
       if (ps != 0xffffffffu) {
@@ -427,7 +447,7 @@ void launch_bucket_sort(const void* keys, const uint16_t* slot, int key_bytes, i
                         int64_t nb, const uint32_t* start, void* kA, uint32_t* vA, void* kB,
                         uint32_t* vB, uint32_t* work, uint32_t* err, int num_sms, cudaStream_t st) {
   const int64_t groups = (n + 3) / 4;
-  const int gA = (int)std::max<int64_t>(1, std::min<int64_t>((groups + kBlock - 1) / kBlock,
+  const int gA = (int)std::max<int64_t>(1, std::min<int64_t>((groups + kBlock * kScatGP - 1) / (kBlock * kScatGP),
                                                              (int64_t)num_sms * 8));
   const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(slot) & 7) == 0;
