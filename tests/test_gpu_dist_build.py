@@ -159,3 +159,35 @@ def test_u64_keys_and_lsd_combine(dvl):
     assert np.array_equal(np.concatenate([c.get_sorted()[0] for c in ctxs]), B.codes)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("M,generic", [(17, False), (3, True)])
+def test_distributed_generic_path_and_width_changes(dvl, M, generic):
+    """M > 16 (the portable update kernels) and the forced generic path in a distributed
+    build; sharded edits at several W on one group (W shrinks and grows)."""
+    lower, level = octree(32, 3, 40 + M)
+    n = len(level)
+    scal = np.random.default_rng(M).standard_normal((M, n)).astype(np.float32)
+    G = 3
+    parts = [np.arange(r, n, G) for r in range(G)]
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts, generic=generic)
+    for e in errs:
+        if e is not None:
+            raise e
+    B = o.build(lower, level, scal)
+    assert np.array_equal(np.concatenate([c.get_sorted()[0] for c in ctxs]), B.codes)
+    tfs = np.stack([synth.random_tf(90 + m, 256, member=m) for m in range(M)])
+    for m in range(M):
+        for c in ctxs:
+            c.update_tf(m, tfs[m])
+    for W in (700, 256, 1024, 5):
+        outs, errs = run_threads([lambda c=c: c.get_polylines(W) for c in ctxs])
+        for err in errs:
+            if err is not None:
+                raise err
+        U = o.update(B, tfs, W)
+        for out in outs:
+            for k in ("count", "t_min", "t_max"):
+                assert np.array_equal(out[k], U.vertices[k]), (W, k)
+    for c in ctxs:
+        c.close()
