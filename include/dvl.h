@@ -127,6 +127,22 @@ typedef struct {
 dvl_status dvl_locate(dvl_ctx *ctx, uint64_t npts, const uint32_t *xyz, int64_t *cell,
                       dvl_mem where);
 
+/* Brushing ("We use the ROIs' first and last Hilbert codes as selection ranges"):
+ * the cells selected by brushing pixels x0..x1 (0 <= x0 <= x1 < W) of the last polylines of
+ * width W are the curve-order range [lo(x0), hi(x1)] of the bin ranges; out4 = {first cell,
+ * last cell (global curve-order indices), the first cell's code, the last cell's code}.  A
+ * sharded context with a communicator calls it collectively (every rank gets both codes);
+ * without one, a code of a cell held by another shard is ~0.  Synchronises.  Errors: STATE
+ * (no polylines of width W yet), INVAL. */
+dvl_status dvl_brush(dvl_ctx *ctx, uint32_t W, uint32_t x0, uint32_t x1, uint64_t *out4);
+
+/* The 3D side of brushing and linking: for each integer point of the logical
+ * grid, 1 if the cell containing it (dvl_locate) has a code in [code_lo, code_hi] (the ROI
+ * as Hilbert codes, from dvl_brush), else 0 (also for points in no cell).  flag: npts int64
+ * in memory space `where`.  Errors: as dvl_locate. */
+dvl_status dvl_roi_contains(dvl_ctx *ctx, uint64_t npts, const uint32_t *xyz, uint64_t code_lo,
+                            uint64_t code_hi, int64_t *flag, dvl_mem where);
+
 /* Milliseconds of the last build / update / get_polylines, measured with CUDA events on
  * the context stream (only with DVL_FLAG_TIMING; otherwise all zero). */
 typedef struct {

@@ -2003,8 +2003,10 @@ dvl_status dvl_get_prefix(dvl_ctx* ctx, uint64_t* Q, dvl_mem where) {
   return DVL_OK;
 }
 
-dvl_status dvl_locate(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t* cell,
-                      dvl_mem where) {
+namespace {
+// point location, or (roi != nullptr: [lo code, hi code] on the host) the ROI test
+dvl_status locate_points(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t* cell,
+                         dvl_mem where, const uint64_t* roi) {
   if (!ctx) return DVL_E_INVAL;
   if (!ctx->built) {
     set_err(ctx, "dvl_locate before dvl_build");
@@ -2017,6 +2019,7 @@ dvl_status dvl_locate(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t*
   if (npts == 0) return DVL_OK;
   uint32_t* dx = nullptr;
   int64_t* dc = nullptr;
+  unsigned long long* dr = nullptr;
   try {
     CK(cudaSetDevice(ctx->device));
     const Dataset& d = ctx->ds;
@@ -2029,20 +2032,81 @@ dvl_status dvl_locate(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t*
       px = dx;
       pc = dc;
     }
+    if (roi) {
+      dr = dalloc<unsigned long long>(ctx, 2);
+      CK(cudaMemcpyAsync(dr, roi, 16, cudaMemcpyHostToDevice, ctx->stream));
+    }
     launch_locate(px, (int64_t)npts, d.b, ctx->d_t1, ctx->d_t2, ctx->nstates, d.keys, d.key_bytes,
-                  d.level_s, d.n, ctx->cell_offset, pc, ctx->stream);
+                  d.level_s, d.n, ctx->cell_offset, pc, ctx->stream, dr);
     CKLAUNCH();
     if (where == DVL_MEM_HOST) {
       CK(cudaMemcpyAsync(cell, dc, 8 * (size_t)npts, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
     }
+    CK(cudaStreamSynchronize(ctx->stream));
   } catch (Fail& f) {
     dfree(ctx, dx);
     dfree(ctx, dc);
+    dfree(ctx, dr);
     return f.s;
   }
   dfree(ctx, dx);
   dfree(ctx, dc);
+  dfree(ctx, dr);
+  return DVL_OK;
+}
+}  // namespace
+
+dvl_status dvl_locate(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, int64_t* cell,
+                      dvl_mem where) {
+  return locate_points(ctx, npts, xyz, cell, where, nullptr);
+}
+
+dvl_status dvl_roi_contains(dvl_ctx* ctx, uint64_t npts, const uint32_t* xyz, uint64_t code_lo,
+                            uint64_t code_hi, int64_t* flag, dvl_mem where) {
+  const uint64_t roi[2] = {code_lo, code_hi};
+  return locate_points(ctx, npts, xyz, flag, where, roi);
+}
+
+dvl_status dvl_brush(dvl_ctx* ctx, uint32_t W, uint32_t x0, uint32_t x1, uint64_t* out4) {
+  if (!ctx || !out4) return DVL_E_INVAL;
+  if (!ctx->built || ctx->last_W != W || W == 0) {
+    set_err(ctx, "no polylines of this width yet");
+    return DVL_E_STATE;
+  }
+  if (x0 > x1 || x1 >= W) {
+    set_err(ctx, "brush: need x0 <= x1 < W");
+    return DVL_E_INVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const Dataset& d = ctx->ds;
+    unsigned long long r[4] = {0, 0, ~0ull, ~0ull};
+    CK(cudaMemcpyAsync(&r[0], ctx->d_bin_lo + x0, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&r[1], ctx->d_bin_hi + x1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    // the codes of the first and the last brushed cell, from the shard that holds each
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t c = r[e];
+      if (c >= ctx->cell_offset && c < ctx->cell_offset + (uint64_t)d.n) {
+        uint64_t k = 0;
+        CK(cudaMemcpyAsync(&k, static_cast<const char*>(d.keys) + (c - ctx->cell_offset) * d.key_bytes,
+                           d.key_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        r[2 + e] = k;
+      }
+    }
+    if (ctx->comm && ctx->sharded) {   // collective: every shard learns both codes
+      Small sm(ctx, 2);
+      sm.put({r[2], r[3]});
+      comm_ck(ctx, ctx->comm->allreduce(sm.d, 2, kU64, kMin, ctx->stream), "all_reduce MIN brush codes");
+      const std::vector<uint64_t> v = sm.get(2);
+      r[2] = v[0];
+      r[3] = v[1];
+    }
+    for (int i = 0; i < 4; ++i) out4[i] = r[i];
+  } catch (Fail& f) {
+    return f.s;
+  }
   return DVL_OK;
 }
 

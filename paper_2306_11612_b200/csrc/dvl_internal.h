@@ -121,7 +121,7 @@ void launch_weights_reduce_tma(bool smem_tab, const UpdParams& p, const TmaPlan&
 void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t1,
                    const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
                    const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
-                   cudaStream_t st);
+                   cudaStream_t st, const unsigned long long* roi = nullptr);
 // dbuild.cu: the distributed build's device steps and splitter rule
 void launch_sample_keys(const void* keys, int key_bytes, int64_t n, int S, unsigned long long* out,
                         cudaStream_t st);

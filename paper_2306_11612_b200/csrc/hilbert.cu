@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kBlock)
 locate_kernel(const uint32_t* __restrict__ xyz, int64_t npts, int b,
               const uint16_t* __restrict__ t1g, const uint16_t* __restrict__ t2g, int nstates,
               const K* __restrict__ keys, const uint8_t* __restrict__ level, int64_t n,
-              uint64_t cell_offset, int64_t* __restrict__ out) {
+              uint64_t cell_offset, int64_t* __restrict__ out, const unsigned long long* roi) {
   extern __shared__ uint16_t s_tab[];
   uint16_t* s_t1 = s_tab;
   uint16_t* s_t2 = s_tab + nstates * 8;
@@ -388,6 +388,11 @@ locate_kernel(const uint32_t* __restrict__ xyz, int64_t npts, int b,
         }
       }
     }
+    // roi (brushing): 1 if the containing cell's code lies in [roi[0], roi[1]]
+    if (roi) {
+      const int64_t c = res - (int64_t)cell_offset;
+      res = res >= 0 && (uint64_t)keys[c] >= roi[0] && (uint64_t)keys[c] <= roi[1] ? 1 : 0;
+    }
     out[h] = res;
   }
 }
@@ -395,17 +400,17 @@ locate_kernel(const uint32_t* __restrict__ xyz, int64_t npts, int b,
 void launch_locate(const uint32_t* xyz, int64_t npts, int b, const uint16_t* d_t1,
                    const uint16_t* d_t2, int nstates, const void* keys, int key_bytes,
                    const uint8_t* level, int64_t n, uint64_t cell_offset, int64_t* out,
-                   cudaStream_t st) {
+                   cudaStream_t st, const unsigned long long* roi) {
   const size_t smem = (size_t)nstates * (8 + 64) * sizeof(uint16_t);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((npts + kBlock - 1) / kBlock, 4096));
   if (key_bytes == 4)
     locate_kernel<uint32_t><<<grid, kBlock, smem, st>>>(xyz, npts, b, d_t1, d_t2, nstates,
                                                         (const uint32_t*)keys, level, n,
-                                                        cell_offset, out);
+                                                        cell_offset, out, roi);
   else
     locate_kernel<unsigned long long><<<grid, kBlock, smem, st>>>(
         xyz, npts, b, d_t1, d_t2, nstates, (const unsigned long long*)keys, level, n, cell_offset,
-        out);
+        out, roi);
 }
 
 __global__ void iota_kernel(uint32_t* v, int64_t n) {

@@ -36,7 +36,7 @@ SYMBOLS = ["dvl_create", "dvl_destroy", "dvl_last_error", "dvl_status_string", "
            "dvl_shard_finish", "dvl_set_timing", "dvl_locate", "dvl_set_level_scale",
            "dvl_nccl_unique_id", "dvl_set_comm", "dvl_local_group_create",
            "dvl_local_group_destroy", "dvl_set_local_comm", "dvl_get_shard",
-           "dvl_select_splitters"]
+           "dvl_select_splitters", "dvl_brush", "dvl_roi_contains"]
 
 VERTEX_DTYPE = np.dtype([("t_min", "<f4"), ("t_max", "<f4"), ("t_mean", "<f4"), ("y", "<f4"),
                          ("r", "<f4"), ("g", "<f4"), ("b", "<f4"), ("count", "<u4")])
@@ -124,6 +124,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvl_set_local_comm": (i32, [P, P, i32]),
         "dvl_get_shard": (i32, [P, ctypes.POINTER(_ShardInfo)]),
         "dvl_select_splitters": (i32, [P, P, i32, i32, P]),
+        "dvl_brush": (i32, [P, u32, u32, u32, P]),
+        "dvl_roi_contains": (i32, [P, u64, P, u64, u64, P, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -423,11 +425,35 @@ class Context:
         self._check(self._lib.dvl_locate(self._h, len(xyz), _ptr(xyz), _ptr(out), HOST), "dvl_locate")
         return out
 
-    def brush(self, W: int, x0: int, x1: int):
-        """The cells (first, last) in curve order selected by brushing pixels x0..x1 of the
-        last polylines of width W."""
-        lo, hi = self.get_bin_ranges(W)
-        return int(lo[x0]), int(hi[x1])
+    def brush(self, W: int, x0: int, x1: int) -> dict:
+        """Brushing pixels x0..x1 of the last polylines of width W: the selected
+        cells' curve-order range (first, last) and the ROI as Hilbert codes (code_first,
+        code_last) -- dvl_brush."""
+        out = np.zeros(4, np.uint64)
+        self._check(self._lib.dvl_brush(self._h, W, x0, x1, _ptr(out)), "dvl_brush")
+        return {"first": int(out[0]), "last": int(out[1]), "code_first": int(out[2]),
+                "code_last": int(out[3])}
+
+    def roi_contains(self, xyz, code_lo: int, code_hi: int):
+        """The 3D side of brushing: 1 where the cell containing the point has a
+        code in [code_lo, code_hi], else 0 (numpy in -> numpy int64; a torch CUDA int32 /
+        uint32 tensor in -> torch CUDA int64) -- dvl_roi_contains."""
+        if _is_device(xyz):
+            import torch
+            _need(xyz.dtype in (torch.int32, torch.uint32) and xyz.numel() % 3 == 0,
+                  "xyz: int32/uint32 tensor of shape (n, 3)")
+            xyz = xyz.contiguous()
+            out = torch.empty(xyz.numel() // 3, dtype=torch.int64, device=xyz.device)
+            self._order_in(xyz, out)
+            self._check(self._lib.dvl_roi_contains(self._h, out.numel(), _ptr(xyz), code_lo, code_hi,
+                                                   _ptr(out), DEVICE), "dvl_roi_contains")
+            self._order_out()
+            return out
+        xyz = np.ascontiguousarray(np.asarray(xyz, dtype=np.uint32).reshape(-1, 3))
+        out = np.empty(len(xyz), np.int64)
+        self._check(self._lib.dvl_roi_contains(self._h, len(xyz), _ptr(xyz), code_lo, code_hi,
+                                               _ptr(out), HOST), "dvl_roi_contains")
+        return out
 
     # ------------------------------------------------------------------ sharding
     def set_comm(self, nranks: int, rank: int, uid: bytes):

@@ -118,6 +118,14 @@ def test_library_distributed_build_and_sharded_edits(dvl, G, kind):
                 assert np.array_equal(out[k], U.vertices[k]) and np.array_equal(out[k], single[k])
             rel = np.abs(out["t_mean"].astype(np.float64) - U.vertices["t_mean"]) / np.maximum(U.vertices["t_mean"], 1e-30)
             assert rel.max() <= 1e-5
+        # brushing on a sharded dataset (collective): every rank gets the ROI's codes
+        brs, errs = run_threads([lambda c=c: c.brush(W, 40, 90) for c in ctxs])
+        for err in errs:
+            if err is not None:
+                raise err
+        for br in brs:
+            assert (br["first"], br["last"]) == (int(U.lo[40]), int(U.hi[90]))
+            assert (br["code_first"], br["code_last"]) == (int(B.codes[br["first"]]), int(B.codes[br["last"]]))
         # each shard's prefix of its own cells (shard-relative) plus the earlier shards' total
         # is the global Q (Eq. 4)
         for c, sh in zip(ctxs, shards):

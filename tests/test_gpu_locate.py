@@ -85,8 +85,11 @@ def test_brush_selects_the_bin_cells(dvl):
     W = 64
     ctx.get_polylines(W)
     lo, hi = ctx.get_bin_ranges(W)
-    first, last = ctx.brush(W, 10, 20)
+    br = ctx.brush(W, 10, 20)
+    first, last = br["first"], br["last"]
     assert (first, last) == (int(lo[10]), int(hi[20]))
+    # the ROI as Hilbert codes: the first and last brushed cells' codes
+    assert (br["code_first"], br["code_last"]) == (int(B.codes[first]), int(B.codes[last]))
     # the brushed cells' centroids locate inside the range, the others outside
     half = ((1 << level.astype(np.int64)) >> 1)[:, None]
     cent = (lower.astype(np.int64) + half).astype(np.uint32)
@@ -96,4 +99,29 @@ def test_brush_selects_the_bin_cells(dvl):
     assert np.array_equal(k, rank)
     inside = (k >= first) & (k <= last)
     assert inside.sum() == last - first + 1
+    ctx.close()
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_roi_contains_matches_oracle(dvl, seed):
+    """dvl_roi_contains (a sample point is in the ROI iff the cell containing it
+    has a code in the ROI's code range) against the oracle's containment test + its codes."""
+    lower, level = octree(32, 3, seed)
+    scal = np.random.default_rng(seed).standard_normal((3, len(level))).astype(np.float32)
+    B = o.build(lower, level, scal)
+    ctx = dvl.Context(device=0)
+    ctx.build(lower, level, scal)
+    W = 100
+    ctx.get_polylines(W)
+    br = ctx.brush(W, 30, 55)
+    U = o.update(B, np.stack([o.identity_tf(256)] * 3), W)
+    assert (br["first"], br["last"]) == (int(U.lo[30]), int(U.hi[55]))
+    rng = np.random.default_rng(seed + 10)
+    pts = rng.integers(0, 33, size=(20000, 3)).astype(np.uint32)   # includes points outside
+    got = ctx.roi_contains(pts, br["code_first"], br["code_last"])
+    idx = o.locate(lower, level, B, pts)
+    ref = np.where(idx >= 0, (B.codes[np.maximum(idx, 0)] >= br["code_first"]) &
+                   (B.codes[np.maximum(idx, 0)] <= br["code_last"]), False).astype(np.int64)
+    assert np.array_equal(got, ref)
+    assert 0 < got.sum() < len(pts)
     ctx.close()
