@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TF-edit DVL update ms & Gcells/s at 1/2/4/8 B200; build (Hilbert+sort) ms"
-CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
+CONFIG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4, "Cpaper": 5}
 
 
 def parse():
@@ -191,6 +191,14 @@ def emit(obj):
 def workload_config(name, n, M, W, N, levels, bits, world, sharded, gbits, n_per_gpu=None):
     """The `config` object of the JSON line (shared by both arms)."""
     ci = CONFIG_INDEX[name]
+    if name == "Cpaper":
+        return {"workload": "Cpaper (not a BASELINE config): shaped like the paper's data, 4 AMR "
+                            "levels, 4 fields with their own ranges (P:403-410, Table 1)",
+                "n_cells": n, "members": M, "W": W, "tf_size": N, "levels": levels, "bits": bits,
+                "edits": "member 0, new random TF per step",
+                "l2": "flushed (256 MiB write) before every timed step",
+                "parallelism": f"sharded-dp{world}" if sharded else "single",
+                "cells_per_gpu": n_per_gpu or n, "global_bits": gbits or bits}
     try:
         with open(os.path.join(ROOT, "BASELINE.json")) as f:
             desc = json.load(f)["configs"][ci]
@@ -556,7 +564,10 @@ def run_native(args, rank, world, local):
         "paper_context": {"value": 0.61, "unit": "Gcells/s", "gpu": "NVIDIA A6000",
                           "workload": "Molecular Cloud, 35.8 M cells x 4 fields, 4 AMR levels",
                           "derived_from": "Table 1 (PAPER.md lines 390-395): 58.6 ms per TF edit",
-                          "note": "context only: another GPU and dataset, not the target"},
+                          "note": "context only: another GPU and dataset, not the target",
+                          **({"edit_ms_here": ms_per_step, "paper_edit_ms": 58.6,
+                              "ratio_paper_over_here": 58.6 / ms_per_step}
+                             if args.config == "Cpaper" else {})},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches,

@@ -217,6 +217,10 @@ CONFIGS = {
     "C3": ("amr", 2048, 4, (0.30, 0.30, 0.30, 0.30), 8, 4096, "per_member", True),
     "C4": ("uniform", 512, 0, (), 16, 1024, "shared", False),
     "C5": ("amr", 4096, 4, (0.32, 0.32, 0.32, 0.32), 4, 1024, "shared", False),
+    # not a BASELINE config: shaped like the paper's evaluation data (Table 1:
+    # 35.8 M cells, 4 AMR levels, 4 fields with their own ranges) for a like-for-like context
+    # number against the paper's 58.6 ms per edit (SURVEY 8(d) "C-paper")
+    "Cpaper": ("amr", 1024, 3, (0.28, 0.275, 0.27), 4, 1024, "per_member", True),
 }
 
 
