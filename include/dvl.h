@@ -191,8 +191,10 @@ dvl_status dvl_build(dvl_ctx *ctx, uint64_t n, const uint32_t *lower_xyz, const 
 
 /* Exponent P in [0, 16] (Eq. 3), minimum importance eps in [0, 1], and the
  * max(V_h) mode.  Defaults 1, 0.025, CONSERVATIVE.  Takes effect at the next
- * dvl_update_tf.  Errors: INVAL (NaN or out of range), RANGE (after a build:
- * ceil(Lmax * P) > 100, fp32 weight overflow, reading A29). */
+ * dvl_update_tf.  EXACT on a shard takes the max over every shard's cells (an all_reduce on
+ * the context's communicator: this call and every TF install are then collective; without
+ * a communicator such a shard fails with STATE).  Errors: INVAL (NaN or out of range),
+ * RANGE (after a build: ceil(Lmax * P) > 100, fp32 weight overflow, reading A29). */
 dvl_status dvl_set_params(dvl_ctx *ctx, float P, float eps, dvl_maxv_mode mode);
 
 /* The level factor of the importance (Eq. 3): the cell width, f = (V/maxV 2^L)^P

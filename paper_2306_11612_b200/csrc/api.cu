@@ -447,6 +447,13 @@ void run_weights(dvl_ctx* ctx, bool export_q, unsigned long long* q_out, int mem
     int grid = (int)(d.n_pad / ((int64_t)kBlock * per));
     launch_maxv_exact(p, ctx->d_maxv, grid, ctx->stream);
     CKLAUNCH();
+    // a shard's exact max(V_h) is the max over every shard's cells: one MAX all_reduce of
+    // the bits (maxV >= +0, so the u32 order is the float order); collective
+    if (ctx->sharded) {
+      if (!ctx->comm) fail(ctx, DVL_E_STATE, "exact max(V_h) on a shard needs the context's communicator");
+      if (const char* e = ctx->comm->allreduce(ctx->d_maxv, 1, kU32, kMax, ctx->stream))
+        fail(ctx, DVL_E_NCCL, std::string("all_reduce MAX of maxV: ") + e);
+    }
   }
   toc(ctx, PH_MAXV);
   // the edit cache: an edit of member e reads only e's scalars and the cached alpha range

@@ -199,3 +199,33 @@ def test_distributed_generic_path_and_width_changes(dvl, M, generic):
                 assert np.array_equal(out[k], U.vertices[k]), (W, k)
     for c in ctxs:
         c.close()
+
+
+def test_distributed_exact_maxv(dvl):
+    """DVL_MAXV_EXACT on shards: max(V_h) over every shard's cells (an all_reduce MAX inside
+    the library; TF installs are then collective), equal to the one-context result."""
+    lower, level = octree(32, 3, 77)
+    n, M, W, G = len(level), 3, 400, 2
+    scal = np.random.default_rng(77).standard_normal((M, n)).astype(np.float32)
+    parts = [np.arange(r, n, G) for r in range(G)]
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts)
+    for e in errs:
+        if e is not None:
+            raise e
+    B = o.build(lower, level, scal)
+    tfs = np.stack([synth.random_tf(300 + m, 256, member=m) for m in range(M)])
+    _, errs = run_threads([lambda c=c: c.set_params(1.0, 0.025, "exact") for c in ctxs])
+    assert all(e is None for e in errs), errs
+    for m in range(M):
+        _, errs = run_threads([lambda c=c, m=m: c.update_tf(m, tfs[m]) for c in ctxs])
+        assert all(e is None for e in errs), errs
+    outs, errs = run_threads([lambda c=c: c.get_polylines(W) for c in ctxs])
+    assert all(e is None for e in errs), errs
+    U = o.update(B, tfs, W, mode="exact")
+    for c in ctxs:
+        assert np.float32(c.info()["maxV"]) == np.float32(U.maxV)
+    for out in outs:
+        for k in ("count", "t_min", "t_max"):
+            assert np.array_equal(out[k], U.vertices[k])
+    for c in ctxs:
+        c.close()
