@@ -107,6 +107,7 @@ cudaError_t prepare_tma_kernels();
 int tma_items_for(int M);
 size_t tma_smem(const TmaPlan& plan);
 cudaError_t debug_stats(unsigned long long* out8, bool reset);
+cudaError_t debug_p1(unsigned long long* out);
 int tma_blocks_per_sm(int M, bool smem_tab, const TmaPlan& plan, int pass);
 int tma_blocks_per_sm_cache(int M, const TmaPlan& plan);
 int tma_tile2_cells(int M);
