@@ -2178,6 +2178,12 @@ extern "C" __attribute__((visibility("default"))) int dvl_debug_bt(unsigned long
 extern "C" __attribute__((visibility("default"))) int dvl_debug_tl2(unsigned long long* out) {
   return dvl::debug_tl2(out) == cudaSuccess ? 0 : 1;
 }
+extern "C" __attribute__((visibility("default"))) int dvl_debug_aw(unsigned long long* out) {
+  return dvl::debug_aw(out) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int dvl_debug_nored(int v) {
+  return dvl::debug_nored(v) == cudaSuccess ? 0 : 1;
+}
 extern "C" __attribute__((visibility("default"))) int dvl_debug_p1(unsigned long long* out) {
   return dvl::debug_p1(out) == cudaSuccess ? 0 : 1;
 }

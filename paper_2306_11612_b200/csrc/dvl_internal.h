@@ -161,7 +161,9 @@ int local_group_size(const LocalGroup* g);
 Comm* make_local_comm(LocalGroup* g, int rank);
 size_t agg_bytes(int M, int64_t nwt);
 cudaError_t debug_tl2(unsigned long long* out);
-cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds   // DVL_PROF builds
+cudaError_t debug_bt(unsigned long long* out);     // DVL_PROF builds
+cudaError_t debug_nored(int v);                    // DVL_PROF builds
+cudaError_t debug_aw(unsigned long long* out);     // DVL_PROF builds
 void launch_agg_build(const UpdParams& p, void* agg, int64_t nwt, int num_sms, cudaStream_t st);
 // blist / bctr (2 x n_pad / 128 u64, 2 u32 zeroed once): the boundary-tile list, used when
 // the pixels outnumber agg_reduce's warps (then a bin_boundary launch follows)

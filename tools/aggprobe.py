@@ -29,7 +29,7 @@ def main():
     out = torch.empty((M, W, 8), dtype=torch.float32, device="cuda")
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     buf = (ctypes.c_ulonglong * (8 + 2048 + 4096))()
-    bt = (ctypes.c_ulonglong * (2048 * 6))()
+    bt = (ctypes.c_ulonglong * (4096 * 6))()
     for it in range(12):
         flush.zero_()
         torch.cuda.synchronize()
@@ -72,6 +72,15 @@ def main():
 
 def phases(bt):
     b = np.array(list(bt), dtype=np.int64).reshape(-1, 6)
+    stride = int(os.environ.get("BT_STRIDE", "0"))   # bin_boundary: a warp's second tile is e + stride
+    if stride:
+        for nm, sl in (("first tiles", b[:min(stride, 4096)]), ("second tiles", b[stride:4096])):
+            s = sl[(sl > 0).all(axis=1)]
+            if len(s):
+                d = np.diff(s, axis=1) / 1e3
+                print("  bin_boundary %s (%d): stage %.2f | weights %.2f | bins %.2f | fold %.2f | mid+flush %.2f us (p50)" % (
+                    (nm, len(s)) + tuple(np.median(d, axis=0))))
+        return
     b = b[(b > 0).all(axis=1)]
     if len(b):
         d = np.diff(b, axis=1) / 1e3

@@ -18,7 +18,8 @@ import synth  # noqa: E402
 SLOTS = 8 + 2048 + 4096
 BASE = SLOTS - 32
 NAMES = [("pass1 entry", 0), ("pass1 after wait", 10), ("pass1 stream end", 11), ("pass1 end", 1),
-         ("agg entry", 2), ("agg after wait", 4), ("agg end", 3)]
+         ("agg entry", 2), ("agg after wait", 4), ("agg end", 3),
+         ("bin_boundary entry", 6), ("bin_boundary after wait", 8), ("bin_boundary end", 7)]
 NAMES2 = [("prologue start", 0), ("prologue end", 1), ("epilogue entry", 2),
           ("epilogue after wait", 4), ("epilogue after wait (last)", 5),
           ("epilogue loads done (last)", 7), ("epilogue vertex done (last)", 6), ("epilogue end", 3)]
@@ -30,6 +31,8 @@ def main():
     W = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
     cfg = synth.make_config(name)
     lib = dvl.load()
+    if os.environ.get("TL_NORED") == "1":   # timing experiment: pass 2 without its atomics
+        lib.dvl_debug_nored(1)
     ctx = dvl.Context(device=0)
     ctx.build(cfg["lower"], cfg["level"], cfg["scal"])
     M = cfg["M"]
