@@ -59,8 +59,8 @@ struct Dataset {
   unsigned long long* meta2 = nullptr;          // n_pad / 128: the warp's running q sum in its
                                                 // pass-1 chunk before the warp tile's tile
   void* agg = nullptr;                          // D3: per warp tile and member t statistics
-  unsigned long long* blist = nullptr;          // 2 x n_pad / 128: listed boundary warp tiles
-  uint32_t* bctr = nullptr;                     // their count + done counter (self-resetting)
+  unsigned long long* blist = nullptr;          // 2 x n_pad / 128: listed boundary warp tiles (+ the job list)
+  uint32_t* bctr = nullptr;                     // their counts + done counters (self-resetting)
   // edit cache (TMA path, M >= 3): per cell the min / max of the alpha bits of the members
   // other than cache_member, valid while their TFs and the domains stay as they were
   uint32_t* cmin = nullptr;
@@ -129,7 +129,7 @@ struct dvl_ctx {
   int64_t* d_export = nullptr;              // the accumulator export, merged in place
   uint64_t export_cap = 0;
   bool edit_cache = true;                 // DVL_FLAG_NO_EDIT_CACHE: every edit reads every member
-  int pass2_mode = 0;                     // 0 auto, 1 boundary tiles inline, 2 listed (flags)
+  int pass2_mode = 0;                     // 0 auto, 1 boundary tiles inline, 2 listed, 3 jobs (flags)
   uint32_t prod_sleep = 1000000;          // producer wait hint (ns)
   int stages_override = 0;
   int dbg = 0;                // experiment: pass-2 ring depth
@@ -661,7 +661,10 @@ dvl_status dvl_create(const dvl_init* init, dvl_ctx** out) {
     CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     // experiment knobs
     ctx->edit_cache = !(init->flags & DVL_FLAG_NO_EDIT_CACHE);
-    ctx->pass2_mode = (init->flags & DVL_FLAG_PASS2_LIST) ? 2 : (init->flags & DVL_FLAG_PASS2_INLINE) ? 1 : 0;
+    ctx->pass2_mode = (init->flags & DVL_FLAG_PASS2_JOBS)   ? 3
+                      : (init->flags & DVL_FLAG_PASS2_LIST)   ? 2
+                      : (init->flags & DVL_FLAG_PASS2_INLINE) ? 1
+                                                              : 0;
 #ifdef DVL_PROF
     // experiment knobs of the profiling build only
     if (const char* e = getenv("DVL_PROD_SLEEP")) ctx->prod_sleep = (uint32_t)atoi(e);
@@ -941,9 +944,12 @@ void alloc_update_state(dvl_ctx* ctx, Dataset& d) {
     d.tile_meta = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
     d.meta2 = dalloc<unsigned long long>(ctx, (size_t)(d.n_pad / tma_warp_tile_cells()));
     d.agg = dalloc<unsigned char>(ctx, agg_bytes(M, d.n_pad / tma_warp_tile_cells()));
-    d.blist = dalloc<unsigned long long>(ctx, 2 * (size_t)(d.n_pad / tma_warp_tile_cells()));
-    d.bctr = dalloc<uint32_t>(ctx, 2);
-    CK(cudaMemsetAsync(d.bctr, 0, 2 * sizeof(uint32_t), st));
+    // the boundary-tile list (2 words per warp tile), then the job list (u32 per job, at
+    // most nwt / 24 + 1 jobs); counters: boundary list count + done, job list count + done
+    const size_t nwt = (size_t)(d.n_pad / tma_warp_tile_cells());
+    d.blist = dalloc<unsigned long long>(ctx, 2 * nwt + nwt / 32 + 2);
+    d.bctr = dalloc<uint32_t>(ctx, 4);
+    CK(cudaMemsetAsync(d.bctr, 0, 4 * sizeof(uint32_t), st));
   }
   CK(cudaMemcpyAsync(d.d_vmin, d.vmin.data(), 4 * M, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d.d_vmax, d.vmax.data(), 4 * M, cudaMemcpyHostToDevice, st));

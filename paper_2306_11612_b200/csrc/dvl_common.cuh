@@ -71,7 +71,7 @@ struct UpdParams {
   const unsigned long long* shard_totals;
   int nshards, shard;
   uint32_t prod_sleep;     // producer's suspend-time hint (ns) while waiting for a free stage
-  int pass2_mode;          // 0 auto, 1 boundary tiles inline, 2 listed (DVL_FLAG_PASS2_*)
+  int pass2_mode;          // 0 auto, 1 boundary tiles inline, 2 listed, 3 jobs (DVL_FLAG_PASS2_*)
   int dbg;                 // DVL_PROF builds only (DVL_DBG): 4 = kernel timeline / phase probes
   // edit cache (repeated TF edits of one member): per cell the min / max of the alpha bits
   // of the members other than cmember (identity 0xffffffff / 0 when there are none)

@@ -24,6 +24,7 @@ FLAG_GENERIC = 2
 FLAG_NO_EDIT_CACHE = 4
 FLAG_PASS2_INLINE = 8
 FLAG_PASS2_LIST = 16
+FLAG_PASS2_JOBS = 64
 FLAG_LSD_SORT = 32
 
 # every symbol include/dvl.h declares (checked by tests/test_abi.py)
@@ -206,7 +207,7 @@ class Context:
                  sort: str = "auto"):
         """torch_allocator: device memory through PyTorch's caching allocator (dvl_init's
         alloc / free callbacks); False: the library's own cudaMallocAsync pool.
-        edit_cache=False / pass2="inline"|"list": test flags selecting among kernels that
+        edit_cache=False / pass2="inline"|"list"|"jobs": test flags selecting among kernels that
         return identical bits (DVL_FLAG_NO_EDIT_CACHE, DVL_FLAG_PASS2_*); sort="lsd" builds
         with the onesweep LSD sort where the bucket sort would apply (DVL_FLAG_LSD_SORT)."""
         self._lib = load()
@@ -217,7 +218,7 @@ class Context:
             init.cuda_stream = stream if isinstance(stream, int) else stream.cuda_stream
         init.flags = (FLAG_TIMING if timing else 0) | (FLAG_GENERIC if generic else 0) \
             | (0 if edit_cache else FLAG_NO_EDIT_CACHE) \
-            | {None: 0, "inline": FLAG_PASS2_INLINE, "list": FLAG_PASS2_LIST}[pass2] \
+            | {None: 0, "inline": FLAG_PASS2_INLINE, "list": FLAG_PASS2_LIST, "jobs": FLAG_PASS2_JOBS}[pass2] \
             | {"auto": 0, "lsd": FLAG_LSD_SORT}[sort]
         self._alloc = _torch_allocator(device) if torch_allocator else None
         if self._alloc is not None:

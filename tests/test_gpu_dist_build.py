@@ -68,14 +68,14 @@ def build_group(dvl, G, lower, level, scal, parts, **kw):
 
 
 @pytest.mark.parametrize("G", [2, 3, 4])
-@pytest.mark.parametrize("kind", ["round_robin", "uneven"])
-def test_library_distributed_build_and_sharded_edits(dvl, G, kind):
+@pytest.mark.parametrize("kind,pass2", [("round_robin", None), ("uneven", None), ("round_robin", "jobs")])
+def test_library_distributed_build_and_sharded_edits(dvl, G, kind, pass2):
     lower, level = octree(64, 3, 20 + G)
     n, M, W = len(level), 4, 300
     rng = np.random.default_rng(G)
     scal = rng.standard_normal((M, n)).astype(np.float32)
     parts = slices(n, G, kind, rng)
-    ctxs, errs = build_group(dvl, G, lower, level, scal, parts)
+    ctxs, errs = build_group(dvl, G, lower, level, scal, parts, pass2=pass2)
     for e in errs:
         if e is not None:
             raise e

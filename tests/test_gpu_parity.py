@@ -22,10 +22,15 @@ def dvl():
 
 
 def make_ctx(dvl, generic=False):
+    """generic: a bool, or a path name of PATHS ("jobs": the TMA path with pass 2 in its
+    many-jobs form, agg_jobs + the job list, forced at any size)."""
+    if isinstance(generic, str):
+        return dvl.Context(device=0, generic=generic == "generic",
+                           pass2="jobs" if generic == "jobs" else None)
     return dvl.Context(device=0, generic=generic)
 
 
-PATHS = ["tma", "generic"]
+PATHS = ["tma", "generic", "jobs"]
 
 
 # ------------------------------------------------------------------------ fixtures
@@ -146,7 +151,7 @@ def test_c1_uniform_64(dvl, path):
     c = synth.make_config("C1")
     tfs = np.stack([synth.tf_edit(1, 0, member=m) for m in range(c["M"])])
     parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"],
-           generic=path == "generic")
+           generic=path)
 
 
 @pytest.mark.parametrize("seed,E,Lmax,M,W", [(1, 32, 3, 4, 1024), (2, 64, 4, 1, 37), (3, 16, 2, 5, 3),
@@ -159,7 +164,7 @@ def test_amr_octrees(dvl, seed, E, Lmax, M, W, path):
     lower, level = octree(E, Lmax, seed)
     scal = scalars(len(level), M, seed)
     tfs = tfs_for(M, 256, 100 + seed)
-    parity(dvl, lower, level, scal, tfs, W, generic=path == "generic")
+    parity(dvl, lower, level, scal, tfs, W, generic=path)
 
 
 @pytest.mark.parametrize("P", [0.0, 1.0, 2.0, 3.0, 0.5, 2.5])
@@ -169,7 +174,7 @@ def test_params(dvl, P, eps, path):
     lower, level = octree(32, 3, 11)
     scal = scalars(len(level), 4, 12)
     tfs = tfs_for(4, 64, 13)
-    parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps, generic=path == "generic")
+    parity(dvl, lower, level, scal, tfs, 512, P=P, eps=eps, generic=path)
 
 
 @pytest.mark.parametrize("P", [0.5, 1.0, 2.0])
@@ -178,7 +183,7 @@ def test_volume_scaled_importance(dvl, P, path):
     """f = (V/maxV 2^3L)^P, the cell-volume variant of Eq. 3."""
     lower, level = octree(32, 3, 90)
     scal = scalars(len(level), 4, 91)
-    parity(dvl, lower, level, scal, tfs_for(4, 256, 92), 700, generic=path == "generic", P=P,
+    parity(dvl, lower, level, scal, tfs_for(4, 256, 92), 700, generic=path, P=P,
            scale="volume")
 
 
@@ -198,7 +203,7 @@ def test_sizes_and_ragged_tails(dvl, n, path):
     scal = scalars(n, 3, n + 1)
     tfs = tfs_for(3, 256, n + 2)
     for W in ((5,) if n == 1 else (1024, 3, 65536)):
-        parity(dvl, lower, level, scal, tfs, W, generic=path == "generic")
+        parity(dvl, lower, level, scal, tfs, W, generic=path)
 
 
 @pytest.mark.parametrize("E,seed", [(4096, 1), (2 ** 21, 2)])
@@ -253,16 +258,17 @@ def test_repeated_edits_and_determinism(dvl):
     ctx.close()
 
 
+@pytest.mark.parametrize("pass2", [None, "jobs"])
 @pytest.mark.parametrize("M", [3, 4, 5, 8, 16])
-def test_edit_cache_sequences(dvl, M):
+def test_edit_cache_sequences(dvl, M, pass2):
     """The edit cache (repeated edits of one member read that member and the cached alpha
     range of the others): edit sequences that switch members, change a domain, reset the
     TFs and change P / eps in between, each checked against the oracle, and against a
-    context with the cache disabled (bit for bit)."""
+    context with the cache disabled and the default pass 2 (bit for bit)."""
     lower, level = octree(32, 3, 60 + M)
     scal = scalars(len(level), M, 61 + M, nan_frac=0.01)
     B = o.build(lower, level, scal)
-    ctx = make_ctx(dvl)
+    ctx = dvl.Context(device=0, pass2=pass2)
     ctx.build(lower, level, scal)
     ref_ctx = dvl.Context(device=0, edit_cache=False)
     ref_ctx.build(lower, level, scal)
@@ -372,7 +378,7 @@ def test_full_size_config(dvl, name, path):
     c = synth.make_config(name)
     tfs = np.stack([synth.tf_edit(2, 0, member=m) for m in range(c["M"])])
     parity(dvl, c["lower"], c["level"], c["scal"], tfs, c["W"], domain=c["domain"],
-           generic=path == "generic")
+           generic=path)
 
 
 
@@ -390,7 +396,7 @@ def test_negative_zero_and_domain_edges(dvl, path):
     scal[2, ::7] = 2.0
     scal[2, 1::7] = -1.0
     dom = np.array([[0.0, 2.0], [0.0, 1.5], [0.0, 2.0]], f32)
-    parity(dvl, lower, level, scal, tfs_for(3, 256, 73), 64, domain=dom, generic=path == "generic")
+    parity(dvl, lower, level, scal, tfs_for(3, 256, 73), 64, domain=dom, generic=path)
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -401,7 +407,7 @@ def test_width_shrinks_then_grows(dvl, path):
     lower, level = octree(32, 3, 81)
     scal = scalars(len(level), 4, 82)
     B = o.build(lower, level, scal)
-    ctx = make_ctx(dvl, path == "generic")
+    ctx = make_ctx(dvl, path)
     ctx.build(lower, level, scal)
     tfs = tfs_for(4, 256, 83)
     for m in range(4):
@@ -435,7 +441,7 @@ def test_maxv_data_index_range(dvl, mode, path):
     tfs[:, -8:, 3] = 1.0
     tfs[:, 8:-8, 3] = np.clip(tfs[:, 8:-8, 3], 0.1, 0.9)
     B, U, g = parity(dvl, lower, level, scal, tfs, 700, mode=mode, domain=[[0.0, 8.0]],
-                     generic=path == "generic")
+                     generic=path)
     lo, _, inv = o.domains(B, [[0.0, 8.0]])
     ij = [o.index_range(float(B.vmin[m]), float(B.vmax[m]), float(lo[m]), float(inv[m]), N) for m in range(M)]
     assert min(i for i, _ in ij) > 8 and max(j for _, j in ij) < N - 9

@@ -74,25 +74,25 @@ def run_sequence(dvl, c, B, edits, modes, config_index):
 def test_c2_full_size_edit_cache_sequence(dvl):
     c, B = dataset("C2", lambda: synth.make_config("C2"))
     assert B.n > 10_000_000
-    run_sequence(dvl, c, B, edits=5, modes=[None, "list"], config_index=1)
+    run_sequence(dvl, c, B, edits=5, modes=[None, "list", "jobs"], config_index=1)
 
 
-def test_c3_recipe_pass2_inline_and_listed(dvl):
+def test_c3_recipe_pass2_inline_listed_and_jobs(dvl):
     c, B = dataset("C3s", lambda: synth.make_config("C3", scale_E=1024))
     assert B.n > 12_000_000 and c["M"] == 8
-    run_sequence(dvl, c, B, edits=2, modes=["inline", "list"], config_index=2)
+    run_sequence(dvl, c, B, edits=2, modes=["inline", "list", "jobs"], config_index=2)
 
 
 def test_c4_recipe_sixteen_members(dvl):
     c, B = dataset("C4s", lambda: synth.make_config("C4", scale_E=256))
     assert B.n == 256 ** 3 and c["M"] == 16
-    run_sequence(dvl, c, B, edits=2, modes=["inline", "list"], config_index=3)
+    run_sequence(dvl, c, B, edits=2, modes=["inline", "list", "jobs"], config_index=3)
 
 
 def test_c5_recipe_u64_keys(dvl):
     c, B = dataset("C5s", lambda: synth.make_config("C5", box=(256, 128, 8)))
     assert B.n > 15_000_000 and B.b == 12 and B.Lmax == 4
-    run_sequence(dvl, c, B, edits=2, modes=[None], config_index=4)
+    run_sequence(dvl, c, B, edits=2, modes=[None, "jobs"], config_index=4)
     ctx = dvl.Context(device=0)
     ctx.build(c["lower"], c["level"], c["scal"])
     assert ctx.info()["key_bytes"] == 8

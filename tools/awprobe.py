@@ -22,6 +22,8 @@ def main():
     c = bench.device_workload(cfg, dev, 2306)
     M, W = c["M"], c["W"]
     lib = dvl.load()
+    if os.environ.get("TL_NORED") == "1":   # timing experiment: pass 2 without its atomics
+        lib.dvl_debug_nored(1)
     ctx = dvl.Context(device=0)
     ctx.build(c["lower"], c["level"], c["scal"])
     base, seq = bench.tf_sequence(cfg, 12, 256, M)
@@ -50,6 +52,12 @@ def main():
         print(f"{cfg}: {len(b)} straddling warps, p50 (us): loads {np.median(d[:, 0]):.2f} | pixel test "
               f"{np.median(d[:, 1]):.2f} | lazy records {np.median(d[:, 2]):.2f} | single-pixel groups "
               f"{np.median(d[:, 3]):.2f} | boundary tiles / list {np.median(d[:, 4]):.2f}")
+    u = a[(a[:, :4] > 0).all(axis=1) & (a[:, 4] == 0)]   # jobs inside one pixel (lazy test)
+    if len(u):
+        d = np.diff(u[:, [0, 1, 3, 2]], axis=1) / 1e3
+        print(f"{cfg}: {len(u)} single-pixel jobs (lazy test), p50 (us): loads {np.median(d[:, 0]):.2f} | "
+              f"pixel test {np.median(d[:, 1]):.2f} | fold + exit {np.median(d[:, 2]):.2f}; p90 fold + exit "
+              f"{np.percentile(d[:, 2], 90):.2f}")
     a = a[(a[:, :3] > 0).all(axis=1)][:, :3]
     t0 = a[:, 0].min()
     st = (a[:, 0] - t0) / 1e3

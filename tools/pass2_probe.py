@@ -23,7 +23,7 @@ base, seq = bench.tf_sequence(cfg, steps + 5, 256, M)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 out = torch.empty(M * W * 8, dtype=torch.int32, device=dev)
 ref = None
-for mode in (None, "inline", "list"):
+for mode in (None, "inline", "list", "jobs"):
     stream = torch.cuda.Stream()
     ctx = dvl.Context(device=0, stream=stream, timing=True, pass2=mode)
     ctx.build(c["lower"], c["level"], c["scal"])

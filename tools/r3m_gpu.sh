@@ -1,0 +1,10 @@
+python paper_2306_11612_b200/build.py --define=DVL_PROF > /dev/null 2>&1 || echo build failed
+DVL_DBG=4 python tools/awprobe.py C2
+DVL_DBG=4 python tools/timeline.py C3 4096 | grep -i "agg\|bin_b\|epilogue end"
+BT_STRIDE=2368 DVL_DBG=4 python tools/aggprobe.py C3 4096 | grep bin_boundary
+python paper_2306_11612_b200/build.py --force > /dev/null 2>&1 || echo build failed
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+for c in C2 C3 C4; do
+python tools/step_probe.py $c ab/old.so 40
+python tools/step_probe.py $c ab/new.so 40
+done

@@ -1,0 +1,4 @@
+python paper_2306_11612_b200/build.py --define=DVL_PROF > /dev/null 2>&1 || echo build failed
+DVL_DBG=4 python tools/awprobe.py C5
+DVL_DBG=4 TL_NORED=1 python tools/awprobe.py C5
+DVL_DBG=4 python tools/awprobe.py C3

@@ -1,0 +1,4 @@
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist_build.py tests/test_gpu_scale.py -x -q 2>&1 | tail -2
+for c in C3 C4 C5; do python tools/pass2_probe.py $c 20; done
+python tools/step_probe.py C3 ab/old.so 30
+python tools/step_probe.py C3 ab/new.so 30
