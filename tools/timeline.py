@@ -19,7 +19,8 @@ SLOTS = 8 + 2048 + 4096
 BASE = SLOTS - 32
 NAMES = [("pass1 entry", 0), ("pass1 after wait", 10), ("pass1 stream end", 11), ("pass1 end", 1),
          ("agg entry", 2), ("agg after wait", 4), ("agg end", 3),
-         ("bin_boundary entry", 6), ("bin_boundary after wait", 8), ("bin_boundary end", 7)]
+         ("bin_boundary entry", 6), ("bin_boundary after wait", 8), ("bin_boundary end", 7),
+         ("agg_jobs entry", 12), ("agg_jobs after wait", 14), ("agg_jobs end", 13)]
 NAMES2 = [("prologue start", 0), ("prologue end", 1), ("epilogue entry", 2),
           ("epilogue after wait", 4), ("epilogue after wait (last)", 5),
           ("epilogue loads done (last)", 7), ("epilogue vertex done (last)", 6), ("epilogue end", 3)]
@@ -33,7 +34,7 @@ def main():
     lib = dvl.load()
     if os.environ.get("TL_NORED") == "1":   # timing experiment: pass 2 without its atomics
         lib.dvl_debug_nored(1)
-    ctx = dvl.Context(device=0)
+    ctx = dvl.Context(device=0, pass2=os.environ.get("TL_PASS2") or None)
     ctx.build(cfg["lower"], cfg["level"], cfg["scal"])
     M = cfg["M"]
     for m in range(M):
