@@ -1590,10 +1590,10 @@ dvl_status dvl_get_polylines(dvl_ctx* ctx, uint32_t W, dvl_vertex* out, dvl_mem 
     // restores the identity of every entry it reads, so all entries stay identity
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
-    if (d.tma)
-      launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
-                          ctx->num_sms, ctx->stream);
+    if (d.tma)   // (1-3 kernels; CKLAUNCH counts one)
+      ctx->launches += launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot, W, a,
+                                         ctx->cell_offset, ctx->d_err, d.tile_meta, d.meta2, d.agg,
+                                         d.blist, d.bctr, ctx->num_sms, ctx->stream) - 1;
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);
@@ -1841,10 +1841,10 @@ dvl_status dvl_shard_reduce(dvl_ctx* ctx, uint32_t W, const uint64_t* totals_dev
     }
     Acc a = cur_acc(ctx);
     tic(ctx, PH_BREDUCE);
-    if (d.tma)
-      launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot_glob, W, a, ctx->cell_offset,
-                        ctx->d_err, d.tile_meta, d.meta2, d.agg, d.blist, d.bctr,
-                          ctx->num_sms, ctx->stream);
+    if (d.tma)   // (1-3 kernels; CKLAUNCH counts one)
+      ctx->launches += launch_agg_reduce(p, pass2_plan(d), d.chunk_prefix, ctx->d_qtot_glob, W, a,
+                                         ctx->cell_offset, ctx->d_err, d.tile_meta, d.meta2, d.agg,
+                                         d.blist, d.bctr, ctx->num_sms, ctx->stream) - 1;
     else
       launch_bin_reduce(d.items, smem_tab_ok(ctx), p, d.tile_prefix, ctx->d_qtot_glob, W, a,
                         ctx->cell_offset, ctx->d_err, d.tiles, ctx->stream);

@@ -167,8 +167,9 @@ cudaError_t debug_aw(unsigned long long* out);     // DVL_PROF builds
 void launch_agg_build(const UpdParams& p, void* agg, int64_t nwt, int num_sms, cudaStream_t st);
 // blist / bctr (2 x n_pad / 128 + n_pad / 4096 + 2 u64, 4 u32 zeroed once): the boundary-tile
 // list, used when the pixels outnumber agg_reduce's warps (then a bin_boundary launch
-// follows), then the straddling-job list of the many-jobs form (agg_jobs + agg_reduce)
-void launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned long long* chunk_prefix,
+// follows), then the straddling-job list of the many-jobs form (agg_jobs + agg_reduce).
+// Returns the number of kernels it launched (1-3).
+int launch_agg_reduce(const UpdParams& p, const TmaPlan& plan, const unsigned long long* chunk_prefix,
                        const unsigned long long* qtot, uint32_t W, const Acc& acc,
                        uint64_t cell_offset, uint32_t* err, const unsigned long long* meta,
                        const unsigned long long* meta2, const void* agg, unsigned long long* blist,

@@ -510,3 +510,23 @@ def test_duplicate_and_overlap_detection_both_sorts(dvl, sort):
         ctx.build(lo3, lv3, scalars(len(lv3), 2, 1))
     assert e.value.status == "DVL_E_OVERLAP"
     ctx.close()
+
+
+@pytest.mark.parametrize("pass2,extra", [("inline", 0), ("list", 1), ("jobs", 2)])
+def test_launch_count_per_edit(dvl, pass2, extra):
+    """dvl_get_timings counts every kernel of an edit (bench.py's gpu_launches): prologue,
+    pass 1, pass 2 (agg_reduce; + bin_boundary when listed; + agg_jobs in the jobs form, whose
+    boundary tiles are listed here: W > pass-1 tiles), epilogue."""
+    lower, level = octree(32, 3, 91)
+    scal = scalars(len(level), 4, 92)
+    tfs = tfs_for(4, 256, 93)
+    ctx = dvl.Context(device=0, pass2=pass2)
+    ctx.build(lower, level, scal)
+    for m in range(4):
+        ctx.update_tf(m, tfs[m])
+    ctx.get_polylines(300)
+    ctx.timings()                      # resets the counter
+    ctx.update_tf(0, synth.tf_edit(9, 1, 256, member=0))
+    ctx.get_polylines(300)
+    assert ctx.timings()["launches"] == 4 + extra
+    ctx.close()
