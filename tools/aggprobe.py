@@ -60,6 +60,7 @@ def main():
     end = (ts[:, 1] - t0) / 1e3
     dur = (ts[:, 1] - ts[:, 0]) / 1e3
     print("warps %d (of the first 2048), with boundary tiles %d" % (len(a), int((nb > 0).sum())))
+    print("  boundary tiles per warp (histogram):", dict(zip(*np.unique(nb, return_counts=True))))
     for nm, x in (("start after first", start), ("loads", loads), ("uniform done", uni),
                   ("total", dur), ("end after first start", end)):
         print("  %-22s p10 %.2f p50 %.2f p90 %.2f max %.2f us" % ((nm,) + tuple(np.percentile(x, [10, 50, 90, 100]))))
