@@ -78,9 +78,10 @@ typedef void (*dvl_free_fn)(void *ptr, size_t bytes, void *cuda_stream, void *us
                                       (default: chosen from W, the tiles and the SM count) */
 #define DVL_FLAG_LSD_SORT 32u      /* build with the onesweep LSD radix sort even where the
                                       bucket sort applies (3b <= 36) */
-#define DVL_FLAG_PASS2_JOBS 64u    /* pass 2 folds the single-pixel jobs 32 per warp and
+#define DVL_FLAG_PASS2_JOBS 64u    /* pass 2 folds the single-pixel jobs several per warp and
                                       takes the others one warp each (default when the
-                                      warp-tile statistics exceed 32 MB) */
+                                      warp-tile statistics exceed 32 MB and there are >= 16
+                                      pass-2 jobs per pixel) */
 
 typedef struct {
     int device;             /* CUDA device ordinal */
