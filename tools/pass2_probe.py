@@ -1,7 +1,7 @@
 """Step time of repeated edits of member 0 under each pass-2 launch mode (stream = the
 persistent default, inline / list = one warp per job), L2 flushed before every step.
 
-usage: python tools/pass2_probe.py [config] [steps]
+usage: python tools/pass2_probe.py [config] [steps] [W] [modes, comma-separated: auto,inline,list,jobs]
 """
 import os
 import statistics
@@ -18,12 +18,15 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 dev = torch.device("cuda", 0)
 c = bench.device_workload(cfg, dev, 2306)
 M, W = c["M"], c["W"]
+if len(sys.argv) > 3:
+    W = int(sys.argv[3])
+modes = [None if m == "auto" else m for m in (sys.argv[4] if len(sys.argv) > 4 else "auto,inline,list,jobs").split(",")]
 n = int(c["level"].shape[0])
 base, seq = bench.tf_sequence(cfg, steps + 5, 256, M)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 out = torch.empty(M * W * 8, dtype=torch.int32, device=dev)
 ref = None
-for mode in (None, "inline", "list", "jobs"):
+for mode in modes:
     stream = torch.cuda.Stream()
     ctx = dvl.Context(device=0, stream=stream, timing=True, pass2=mode)
     ctx.build(c["lower"], c["level"], c["scal"])
@@ -60,8 +63,8 @@ for mode in (None, "inline", "list", "jobs"):
     if ref is None:
         ref = res
     same = (res.view("u1") == ref.view("u1")).all()
-    print(f"{cfg} pass2={mode or 'stream'}: step median {statistics.median(t):.1f} us "
+    print(f"{cfg} W={W} pass2={mode or 'auto'}: step median {statistics.median(t):.1f} us "
           f"({n / statistics.median(t) / 1e3:.1f} Gcells/s) | " +
           " ".join(f"{k[:-3]} {statistics.median(v):.1f}" for k, v in kern.items()) +
-          f" | same bits as stream: {bool(same)}", flush=True)
+          f" | same bits as the first mode: {bool(same)}", flush=True)
     ctx.close()
